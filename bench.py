@@ -1,0 +1,392 @@
+"""Benchmark: integral image + window sum on the BASELINE.json headline config.
+
+Workload (BASELINE.json `metric`, configs[4] = C5): a 70,000 x 85,000 uint8
+binary mask (5.95 Gpx; seeded synthetic stand-in, paper_2410_16291_b200/synthetic.py),
+integral image (uint64/int64) + window sum w=256 stride 1 (69,745 x 84,745
+uint64 outputs).  One step = one pass of the hot path over the whole image:
+
+  table pipeline (headline `value`): ssb_sat_build (table written to HBM)
+  then ssb_window_eval (corner sweep) -- the reference's swa_integral /
+  swa_parallel structure (pkg/src/satsweep/integral.py:192-196).
+
+`value` is device-resident throughput (input already in HBM, outputs
+preallocated, inputs 5.95 GB >> 126 MB L2, so no flush is needed); `e2e` runs
+the public API with pinned host buffers (host->device input copy and
+device->host result copy inside every timed step).  `--impl reference` times
+the reference algorithm (the numpy port under oracle/, all host threads) on a
+bounded band of the same workload.
+
+Multi-GPU: `python -m torch.distributed.run --nproc-per-node N bench.py --gpus N`
+shards output rows across ranks (strong scaling of the fixed image); each rank
+receives its (w-1)-row halo over NCCL inside the timed step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+ROWS, COLS, W = 70000, 85000, 256
+METRIC = "Gpixels/s (integral image + window sum) at 70k×85k; % HBM roofline; 1/2/4/8 GPU"
+UNIT = "Gpixels/s"
+
+
+def peaks() -> dict:
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3]) if v.lower().startswith("active")})
+        loaded = [r for r in rows if r[2] > 300.0] or rows
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(r[2] for r in rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def emit(obj: dict) -> None:
+    print(json.dumps(obj), flush=True)
+
+
+def cpu_port_band(out_rows: int, threads: int = 0):
+    """Reference algorithm (oracle port) on output rows [0, out_rows) of C5; returns (seconds, pixels)."""
+    from oracle import satsweep_oracle as oracle
+    from paper_2410_16291_b200 import synthetic
+
+    band = synthetic.c5(0, out_rows + W - 1)
+    t0 = time.perf_counter()
+    res = oracle.swa_threaded(band, W, "sum", 1, threads or (os.cpu_count() or 1))
+    dt = time.perf_counter() - t0
+    del res
+    # pixel credit: the band's own output rows' share of the image (halo rows are overhead)
+    return dt, out_rows * COLS
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    out_rows = args.ref_rows
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, px = cpu_port_band(out_rows, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    v = px / t / 1e9
+    sample = (f"C5 band of {out_rows} output rows x {COLS} cols ({out_rows + W - 1} input rows) per step; "
+              f"oracle/satsweep_oracle.swa_threaded (numpy restatement of satsweep.swa_parallel)")
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+          "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+          "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded C5 recipe)",
+          "config": {"workload": "C5 70000x85000 u8, integral image + window sum w=256 stride 1",
+                     "sample_rows": out_rows},
+          "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+# ----------------------------------------------------------------------------- our arm
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-rows", type=int, default=4096, help="output rows per reference/CPU step")
+    ap.add_argument("--cpu-rows", type=int, default=8192, help="output rows of the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--rows", type=int, default=ROWS, help="(debug) smaller image")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    from paper_2410_16291_b200 import _device, _engine, _lib, shard, synthetic
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    rows = args.rows
+    kind = ElemKind.U8
+
+    # ---- inputs: this rank's owned rows, generated on the host, copied once (untimed)
+    a_own, b_own = shard.window_input_bands(rows, W, 1, world)[rank]
+    t_gen = time.perf_counter()
+    host_band = synthetic.c5(a_own, b_own) if rows == ROWS else synthetic.bernoulli_rows(5, rows, COLS, 0.01, a_own, b_own)
+    gen_s = time.perf_counter() - t_gen
+    x_own = _device.to_device(host_band, dev)
+    del host_band
+    need = shard.window_needed_rows(rows, W, 1, world)[rank]
+    nr = need[1] - need[0]
+    out_lo, out_hi = shard.output_partition(rows - W + 1, world)[rank]
+    n_out = out_hi - out_lo
+    out_c = COLS - W + 1
+    ld = _engine.sat_ld_for(COLS)
+    sat = _device.empty((nr + 1, ld), np.uint64, dev, "table")
+    out = _device.empty((n_out, out_c), np.uint64, dev, "result")
+    ws_bytes = int(lib.ssb_sat_workspace_bytes(kind.abi_code, nr, COLS, 0))
+    ws = _device.empty((ws_bytes,), np.uint8, dev, "workspace")
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+
+    def get_x():
+        if world == 1:
+            return x_own
+        return shard.halo_exchange(x_own, rows, W, 1, group)
+
+    ev = {k: [] for k in ("prep", "fin", "eval", "end")}
+
+    def step(record: bool):
+        x = get_x()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(lib.ssb_sat_prepare(x.data_ptr(), kind.abi_code, nr, COLS, COLS, 0, ws.data_ptr(), ws_bytes,
+                                       None, None, None, sptr))
+        e1.record(stream)
+        _lib.check(lib.ssb_sat_finish(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), None, ld, None,
+                                      None, ws.data_ptr(), ws_bytes, sptr))
+        e2.record(stream)
+        _lib.check(lib.ssb_window_eval(sat.data_ptr(), None, kind.abi_code, nr, COLS, ld, W, 1, _lib.SUM,
+                                       out.data_ptr(), None, None, out_c, sptr))
+        e3.record(stream)
+        if record:
+            ev["prep"].append((e0, e1))
+            ev["fin"].append((e1, e2))
+            ev["eval"].append((e2, e3))
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    launches0 = _lib.launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        stop.record(stream)
+        barrier()
+    launches = _lib.launch_count() - launches0
+    ms_total = start.elapsed_time(stop)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    phase_ms = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in ev.items() if v}
+
+    # ---- algorithmic bytes: in + table write | table read + out write
+    px_in = nr * COLS
+    tab_bytes = (nr + 1) * (COLS + 1) * 8
+    out_bytes = n_out * out_c * 8
+    kernels = {
+        "sat_prepare (reduce + carries)": (px_in, phase_ms["prep"]),
+        "sat_scan (table write)": (px_in + tab_bytes, phase_ms["fin"]),
+        "window_eval (corner sweep)": (tab_bytes + out_bytes, phase_ms["eval"]),
+    }
+    pk = peaks()
+    dom = max(kernels, key=lambda k: kernels[k][1])
+    dom_bytes, dom_ms = kernels[dom]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tfile = REPO / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(dom.split(" ")[0])
+    b_mat = px_in + 2 * tab_bytes + out_bytes
+    value = rows * COLS / (ms_step * 1e-3) / 1e9
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded C5 recipe, synthetic.py)",
+        "config": {"workload": "C5 70000x85000 u8 mask, integral image (u64) + window sum w=256 stride 1",
+                   "pipeline": "table (ssb_sat_build -> ssb_window_eval)", "parallelism": f"rowband{world}",
+                   "l2": "inputs 5.95 GB >> 126 MB L2; no flush needed", "gen_s": round(gen_s, 1)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": dom,
+                     "peak_source": pk["source"]},
+        "pipeline_roofline": {"bytes_per_step": b_mat, "achieved_gbs": b_mat / (ms_step * 1e-3) / 1e9,
+                              "frac": b_mat / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]},
+        "phases_ms": phase_ms,
+        "phase_gbs": {k: b / (ms * 1e-3) / 1e9 for k, (b, ms) in kernels.items()},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    # ---- fused pipeline on the same resident input (no table)
+    try:
+        x = get_x()
+
+        def fused_step():
+            _lib.check(lib.ssb_window_fused(x.data_ptr(), kind.abi_code, nr, COLS, COLS, W, _lib.SUM,
+                                            out.data_ptr(), None, None, out_c, None, 0, sptr))
+
+        for _ in range(3):
+            fused_step()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            fused_step()
+        f1.record(stream)
+        barrier()
+        fms = f0.elapsed_time(f1) / args.steps
+        fb = px_in + out_bytes
+        result["fused"] = {"value": rows * COLS / (fms * 1e-3) / 1e9, "ms_per_step": fms,
+                           "roofline_frac": fb / (fms * 1e-3) / 1e9 / pk["hbm_gbs"], "bytes_per_step": fb}
+    except Exception as exc:  # pragma: no cover - reporting only
+        result["fused"] = {"error": str(exc)}
+
+    # ---- e2e through the public API with pinned host buffers (rank-local band)
+    if not args.no_e2e and world == 1:
+        try:
+            del sat, ws
+            torch.cuda.empty_cache()
+            host_in = torch.empty((rows, COLS), dtype=torch.uint8, pin_memory=True)
+            _copy_chunks(host_in, x_own)
+            host_out = torch.empty((rows - W + 1, out_c), dtype=torch.int64, pin_memory=True)
+            import paper_2410_16291_b200 as sb
+
+            hin = host_in.numpy()
+            hout = host_out.numpy().view(np.uint64)
+            sb.swa(hin, W, "sum", pipeline="table", out=hout)  # warm-up
+            times = []
+            for _ in range(args.e2e_steps):
+                t0 = time.perf_counter()
+                sb.swa(hin, W, "sum", pipeline="table", out=hout)
+                times.append(time.perf_counter() - t0)
+            te = sum(times) / len(times)
+            result["e2e"] = {"value": rows * COLS / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": rows * COLS,
+                             "d2h_bytes_per_step": (rows - W + 1) * out_c * 8, "s_per_step": te,
+                             "api": "paper_2410_16291_b200.swa(numpy pinned, 256, 'sum', pipeline='table', out=pinned)"
+                                    " -> ssb_swa_host"}
+        except Exception as exc:  # pragma: no cover
+            result["e2e"] = {"error": str(exc)}
+
+    # ---- CPU baseline: the reference algorithm on a bounded band, rank 0 at N=1
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            dt, px = cpu_port_band(args.cpu_rows)
+            result["cpu_baseline"] = {
+                "value": px / dt / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                "sample": f"C5 output rows [0, {args.cpu_rows}) ({args.cpu_rows + W - 1} input rows x {COLS}); "
+                          "oracle.swa_threaded = numpy restatement of satsweep.swa_parallel; "
+                          f"{dt:.1f} s"}
+        except Exception as exc:  # pragma: no cover
+            result["cpu_baseline"] = {"error": str(exc)}
+
+    if rank == 0:
+        emit(result)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def _copy_chunks(dst_host, src_dev, rows_per=4096):
+    for a in range(0, src_dev.shape[0], rows_per):
+        dst_host[a:a + rows_per].copy_(src_dev[a:a + rows_per].cpu())
+
+
+if __name__ == "__main__":
+    main()

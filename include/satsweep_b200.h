@@ -1,0 +1,146 @@
+/*
+ * satsweep_b200.h -- C ABI of the B200-native integral-image / sliding-window
+ * engine (libsatsweep_b200.so).
+ *
+ * The reference (`satsweep`, /root/reference/pkg) is a pure-Python package
+ * with no native ABI; its hot path is reached through these Python call
+ * sites, each of which one entry point below replaces:
+ *
+ *   ssb_sat_build        build_sat / build_sat_parallel
+ *                        (pkg/src/satsweep/integral.py:109-116, parallel.py:106-121)
+ *   ssb_sat_prepare +    the same, split so a row-band shard can exchange its
+ *   ssb_sat_finish       column totals before writing
+ *   ssb_window_eval      sweep_window_sums + finalize
+ *                        (integral.py:141-163, :178-189; stats.py:35-74)
+ *   ssb_window_eval_multi swa_multi_window (integral.py:199-210)
+ *   ssb_window_fused     swa_integral / swa_parallel for stride 1 without a
+ *                        materialised table (integral.py:192-196, parallel.py:137-149)
+ *   ssb_window_sum_at    window_sum (integral.py:119-130)
+ *   ssb_swa_host         api.swa with host buffers (api.py:28-55): host->device
+ *                        copies, compute, device->host copies, streamed by bands
+ *
+ * Conventions
+ *   - Every device pointer is caller-allocated device memory; the library keeps
+ *     no persistent allocations (ssb_swa_host allocates and frees its own
+ *     staging per call).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device entry
+ *     points are asynchronous on that stream.
+ *   - Tables are (rows+1) x (cols+1) with a zero border row/column and row
+ *     pitch `sat_ld` elements; `sat_ld` must be even and the table 16-byte
+ *     aligned.  Integer tables are uint64 modulo 2^64, float tables double.
+ *   - Returns SSB_OK or an error code; ssb_last_error() gives a thread-local
+ *     message.  No entry point falls back to a CPU implementation.
+ */
+#ifndef SATSWEEP_B200_H
+#define SATSWEEP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSB_ABI_VERSION 1
+
+/* status codes */
+#define SSB_OK 0
+#define SSB_EINVAL 1       /* bad argument (InvalidWindowError / ValueError side) */
+#define SSB_ECUDA 2        /* CUDA runtime error */
+#define SSB_ENOMEM 3       /* device or pinned allocation failed (ResourceLimitError) */
+#define SSB_EUNSUPPORTED 4 /* valid request this build does not implement (TypeError side) */
+#define SSB_ENONFINITE 5   /* F32 input holds NaN/Inf (GridValidationError, grid.py:82-83) */
+
+/* element kinds (grid.py:17-46 ElemKind; I32 is an extension for BASELINE C2) */
+#define SSB_U8 0
+#define SSB_U16 1
+#define SSB_I32 2
+#define SSB_F32 3
+
+/* statistic bits (grid.py:49-61 StatKind); several may be requested at once */
+#define SSB_SUM 1
+#define SSB_MEAN 2
+#define SSB_STD 4
+
+/* pipelines for ssb_swa_host */
+#define SSB_PIPE_TABLE 0 /* build table(s) in HBM, then evaluate corners */
+#define SSB_PIPE_FUSED 1 /* never materialise the table (stride 1 only) */
+
+int ssb_abi_version(void);
+const char* ssb_last_error(void);
+
+/* Scratch bytes needed by ssb_sat_prepare/finish/build (carry vectors). */
+int64_t ssb_sat_workspace_bytes(int in_dtype, int64_t rows, int64_t cols, int with_squares);
+
+/* Tiling of the table build: info4 = {strip width (table cols), segment
+ * height (table rows), number of strips, number of segments}.  Used for the
+ * WriteCensus analogue (parallel.py:35-51). */
+int ssb_sat_plan(int in_dtype, int64_t rows, int64_t cols, int with_squares, int64_t* info4);
+
+/* Phase 1+2: reads the image once, fills the workspace.  If `band_totals`
+ * (cols+1 entries, device) is non-NULL it receives the last table row of this
+ * image *without* any carry -- the per-band column-total vector exchanged
+ * between row-band shards.  `nonfinite_flag` (device int, nullable) is OR-ed
+ * with 1 if an F32 pixel is NaN/Inf (grid.py:82-83). */
+int ssb_sat_prepare(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int with_squares,
+                    void* ws, int64_t ws_bytes, void* band_totals, void* band_totals_sq, int* nonfinite_flag,
+                    void* stream);
+
+/* Phase 3: writes the table(s); `sat` may be NULL when only the squared
+ * table is wanted (build_sat(img, squared=True)).  `carry`/`carry_sq` (cols+1 entries, nullable)
+ * are added to every table row: row 0 becomes `carry`, i.e. the global table
+ * row above this band. */
+int ssb_sat_finish(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                   void* sat_sq, int64_t sat_ld, const void* carry, const void* carry_sq, void* ws,
+                   int64_t ws_bytes, void* stream);
+
+/* prepare + finish. */
+int ssb_sat_build(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat, void* sat_sq,
+                  int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, int64_t ws_bytes,
+                  int* nonfinite_flag, void* stream);
+
+/* Window statistics from table(s) of a rows x cols image.  `sat_sq` is needed
+ * iff SSB_STD is requested.  Output dtypes: sum = uint64 for U8/U16, int64 for
+ * I32, double for F32; mean/std = double.  `out_ld` is the output row pitch
+ * in elements.  Output dims: ((rows-w)/stride+1) x ((cols-w)/stride+1). */
+int ssb_window_eval(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols, int64_t sat_ld,
+                    int64_t w, int64_t stride, int stat_mask, void* out_sum, double* out_mean, double* out_std,
+                    int64_t out_ld, void* stream);
+
+/* Several window sizes (stride 1) from one set of tables. */
+int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols,
+                          int64_t sat_ld, int n_windows, const int64_t* windows, int stat_mask,
+                          void* const* out_sums, double* const* out_means, double* const* out_stds,
+                          const int64_t* out_lds, void* stream);
+
+/* Stride-1 window statistics straight from the image.  `segments` = number of
+ * row segments (0 = automatic). */
+int ssb_window_fused(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
+                     int stat_mask, void* out_sum, double* out_mean, double* out_std, int64_t out_ld,
+                     int* nonfinite_flag, int segments, void* stream);
+
+/* Largest window ssb_window_fused accepts. */
+int64_t ssb_window_fused_max_w(void);
+
+/* One four-corner lookup (window_sum); `out_value` is HOST memory receiving a
+ * uint64 (integer table) or double (float table).  Synchronises `stream`. */
+int ssb_window_sum_at(const void* sat, int is_float_table, int64_t rows, int64_t cols, int64_t sat_ld, int64_t top,
+                      int64_t left, int64_t w, void* out_value, void* stream);
+
+/* End-to-end with HOST buffers: input rows x cols at pitch in_ld (elements),
+ * outputs at pitch out_ld.  Streams output-row bands through the device
+ * (each band builds its own local table; offsets cancel) with
+ * copies overlapped on two streams.  Pinned host buffers give full PCIe
+ * bandwidth; pageable ones work but are slower.  `band_rows` = output rows per
+ * band (0 = automatic). */
+int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
+                 int64_t stride, int stat_mask, void* out_sum_host, double* out_mean_host, double* out_std_host,
+                 int64_t out_ld, int pipeline, int device, int64_t band_rows);
+
+/* Count of kernel launches the library issued since load (diagnostics). */
+int64_t ssb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SATSWEEP_B200_H */

@@ -1,0 +1,87 @@
+"""Device plumbing: torch owns device memory and streams; the kernels are ours.
+
+torch is used only for allocation, the current stream and host<->device copies
+of small objects; every computation on the hot path is a launch inside
+libsatsweep_b200.so.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import ResourceLimitError, SatsweepError
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def require_cuda() -> None:
+    t = torch()
+    if not t.cuda.is_available():
+        raise SatsweepError("no CUDA device is available; satsweep-b200 has no CPU fallback")
+
+
+def current_device():
+    require_cuda()
+    t = torch()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr(device=None) -> int:
+    t = torch()
+    return int(t.cuda.current_stream(device).cuda_stream)
+
+
+# storage dtypes: kernels only see raw pointers, so uint16 travels as int16 and
+# uint64 as int64 (bit-identical views on the host side).
+def storage_dtype(np_dtype: np.dtype):
+    t = torch()
+    return {
+        np.dtype(np.uint8): t.uint8,
+        np.dtype(np.uint16): t.int16,
+        np.dtype(np.int32): t.int32,
+        np.dtype(np.float32): t.float32,
+        np.dtype(np.uint64): t.int64,
+        np.dtype(np.int64): t.int64,
+        np.dtype(np.float64): t.float64,
+    }[np.dtype(np_dtype)]
+
+
+def empty(shape, np_dtype, device, what: str):
+    """Device allocation that raises ResourceLimitError (integral.py:76-83) on failure."""
+    t = torch()
+    nbytes = int(np.prod(shape, dtype=object)) * np.dtype(np_dtype).itemsize
+    free, total = t.cuda.mem_get_info(device)
+    if nbytes > total:
+        raise ResourceLimitError(nbytes, what)
+    try:
+        return t.empty(tuple(int(s) for s in shape), dtype=storage_dtype(np_dtype), device=device)
+    except (t.cuda.OutOfMemoryError, RuntimeError) as exc:  # pragma: no cover - device dependent
+        if isinstance(exc, t.cuda.OutOfMemoryError) or "out of memory" in str(exc):
+            raise ResourceLimitError(nbytes, what) from None
+        raise
+
+
+def to_device(arr: np.ndarray, device):
+    """Host raster -> device tensor (one copy)."""
+    t = torch()
+    src = t.from_numpy(np.ascontiguousarray(arr).view(_view_np(arr.dtype)))
+    return src.to(device)
+
+
+def _view_np(dt):
+    dt = np.dtype(dt)
+    return {np.dtype(np.uint16): np.int16, np.dtype(np.uint64): np.int64}.get(dt, dt)
+
+
+def to_host(tensor, np_dtype: np.dtype) -> np.ndarray:
+    """Device tensor -> fresh host numpy array of the requested dtype (bit view)."""
+    return tensor.cpu().numpy().view(np.dtype(np_dtype))
+
+
+def as_np_view(tensor, np_dtype):
+    """Device tensor with a different logical dtype (e.g. int64 storage read as uint64) -- host copy."""
+    return to_host(tensor, np_dtype)

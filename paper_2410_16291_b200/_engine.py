@@ -1,0 +1,167 @@
+"""Device-side orchestration of the CUDA kernels (tables, corner sweep, fused path).
+
+Every function here launches work from libsatsweep_b200.so on the current
+torch stream; nothing computes on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _device, _lib
+from .grid import ElemKind, ImageGrid, StatKind
+
+STAT_ORDER = (StatKind.SUM, StatKind.MEAN, StatKind.STD)
+
+
+def stat_mask(stats) -> int:
+    m = 0
+    for s in stats:
+        m |= s.bit
+    return m
+
+
+def result_dtype(kind: ElemKind, stat: StatKind) -> np.dtype:
+    """stats.py:49-74: integer SUM keeps exact integers, everything else float64."""
+    return kind.sum_dtype if stat is StatKind.SUM else np.dtype(np.float64)
+
+
+def sat_ld_for(cols: int) -> int:
+    """Row pitch of a device table: even (16-byte aligned rows), >= cols + 1."""
+    return (cols + 2) & ~1
+
+
+def device_input(img: ImageGrid):
+    """Return (device tensor, device) for an ImageGrid, copying host rasters once."""
+    if img.on_device:
+        return img.values, img.values.device
+    dev = _device.current_device()
+    return _device.to_device(img.values, dev), dev
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+def check_nonfinite(flag) -> None:
+    if flag is not None and int(flag.item()) != 0:
+        _lib.check(_lib.ENONFINITE)
+
+
+def new_flag(device):
+    t = _device.torch()
+    return t.zeros(1, dtype=t.int32, device=device)
+
+
+def build_tables(x, kind: ElemKind, rows: int, cols: int, device, *, squared: bool, plain: bool = True,
+                 carry=None, carry_sq=None, flag=None):
+    """Build the (rows+1) x (cols+1) table(s) in HBM.  Returns (sat, sat_sq, sat_ld).
+
+    ``plain=False`` with ``squared=True`` builds only the squared table (build_sat(img, squared=True))."""
+    lib = _lib.load()
+    ld = sat_ld_for(cols)
+    acc_dt = np.float64 if kind is ElemKind.F32 else np.uint64
+    sat = sq = None
+    if plain:
+        sat = _device.empty((rows + 1, ld), acc_dt, device, f"a {rows + 1}x{cols + 1} integral table")
+    if squared:
+        sq = _device.empty((rows + 1, ld), acc_dt, device, f"a {rows + 1}x{cols + 1} integral table")
+    ws_bytes = int(lib.ssb_sat_workspace_bytes(kind.abi_code, rows, cols, 1 if squared else 0))
+    ws = _device.empty((max(ws_bytes, 8),), np.uint8, device, "table workspace")
+    st = _device.stream_ptr(device)
+    rc = lib.ssb_sat_build(_ptr(x), kind.abi_code, rows, cols, cols, _ptr(sat), _ptr(sq), ld, _ptr(carry),
+                           _ptr(carry_sq), _ptr(ws), ws_bytes, _ptr(flag), st)
+    _lib.check(rc, "build_sat", (rows + 1) * (cols + 1) * 8)
+    return sat, sq, ld
+
+
+def alloc_outputs(kind: ElemKind, stats, out_r: int, out_c: int, device):
+    return {s: _device.empty((out_r, out_c), result_dtype(kind, s), device, f"a {out_r}x{out_c} result grid")
+            for s in stats}
+
+
+def eval_tables(sat, sq, ld: int, kind: ElemKind, rows: int, cols: int, w: int, stride: int, stats, device,
+                outs=None):
+    """Corner sweep + fused finalize for every requested stat in one launch."""
+    lib = _lib.load()
+    out_r, out_c = (rows - w) // stride + 1, (cols - w) // stride + 1
+    outs = outs or alloc_outputs(kind, stats, out_r, out_c, device)
+    o_sum, o_mean, o_std = (outs.get(StatKind.SUM), outs.get(StatKind.MEAN), outs.get(StatKind.STD))
+    rc = lib.ssb_window_eval(_ptr(sat), _ptr(sq), kind.abi_code, rows, cols, ld, w, stride, stat_mask(stats),
+                             _ptr(o_sum), _ptr(o_mean), _ptr(o_std), out_c, _device.stream_ptr(device))
+    _lib.check(rc, "window evaluation")
+    return outs
+
+
+def fused(x, kind: ElemKind, rows: int, cols: int, w: int, stats, device, flag=None, outs=None, segments: int = 0):
+    lib = _lib.load()
+    out_r, out_c = rows - w + 1, cols - w + 1
+    outs = outs or alloc_outputs(kind, stats, out_r, out_c, device)
+    o_sum, o_mean, o_std = (outs.get(StatKind.SUM), outs.get(StatKind.MEAN), outs.get(StatKind.STD))
+    rc = lib.ssb_window_fused(_ptr(x), kind.abi_code, rows, cols, cols, w, stat_mask(stats), _ptr(o_sum),
+                              _ptr(o_mean), _ptr(o_std), out_c, _ptr(flag), segments, _device.stream_ptr(device))
+    _lib.check(rc, "fused window evaluation")
+    return outs
+
+
+def fused_max_w() -> int:
+    return int(_lib.load().ssb_window_fused_max_w())
+
+
+def choose_pipeline(pipeline: str, kind: ElemKind, w: int, stride: int) -> str:
+    if pipeline not in ("auto", "table", "fused"):
+        raise ValueError(f"unknown pipeline {pipeline!r}; expected auto, table, or fused")
+    fusable = stride == 1 and w <= fused_max_w()
+    if pipeline == "fused":
+        if not fusable:
+            raise ValueError("the fused pipeline needs stride 1 and w <= %d" % fused_max_w())
+        return "fused"
+    if pipeline == "table":
+        return "table"
+    # auto: integer results are exact on both pipelines, so take the cheaper
+    # one; float results keep the table pipeline so swa/multi_window/swa_integral
+    # agree bit for bit (integral.py:199-204).
+    return "fused" if (fusable and kind.is_integer) else "table"
+
+
+def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None):
+    """All requested stats for one window on the device; returns {StatKind: tensor}."""
+    x, dev = device_input(img)
+    rows, cols = img.rows, img.cols
+    pipe = choose_pipeline(pipeline, img.elem_kind, w, stride)
+    flag = new_flag(dev) if img.elem_kind is ElemKind.F32 else None
+    if pipe == "fused":
+        res = fused(x, img.elem_kind, rows, cols, w, stats, dev, flag=flag, outs=outs)
+    else:
+        need_sq = StatKind.STD in stats
+        sat, sq, ld = build_tables(x, img.elem_kind, rows, cols, dev, squared=need_sq, flag=flag)
+        res = eval_tables(sat, sq, ld, img.elem_kind, rows, cols, w, stride, stats, dev, outs=outs)
+    check_nonfinite(flag)
+    return res
+
+
+def run_host(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None, band_rows: int = 0):
+    """Host raster in, host results out, through the C-ABI streaming entry point ssb_swa_host."""
+    lib = _lib.load()
+    _device.require_cuda()
+    kind = img.elem_kind
+    pipe = choose_pipeline(pipeline, kind, w, stride)
+    rows, cols = img.rows, img.cols
+    out_r, out_c = (rows - w) // stride + 1, (cols - w) // stride + 1
+    if outs is None:
+        outs = {s: np.empty((out_r, out_c), dtype=result_dtype(kind, s)) for s in stats}
+    for s, a in outs.items():
+        if a.shape != (out_r, out_c) or a.dtype != result_dtype(kind, s) or not a.flags.c_contiguous:
+            raise ValueError(f"out[{s.value}] must be a C-contiguous {result_dtype(kind, s)} array of shape "
+                             f"{(out_r, out_c)}")
+    src = img.values
+    ptr = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    t = _device.torch()
+    rc = lib.ssb_swa_host(src.ctypes.data_as(ctypes.c_void_p), kind.abi_code, rows, cols, cols, w, stride,
+                          stat_mask(stats), ptr(outs.get(StatKind.SUM)), ptr(outs.get(StatKind.MEAN)),
+                          ptr(outs.get(StatKind.STD)), out_c, _lib.PIPE_FUSED if pipe == "fused" else _lib.PIPE_TABLE,
+                          t.cuda.current_device(), band_rows)
+    _lib.check(rc, "swa")
+    return outs

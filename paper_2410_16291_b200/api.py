@@ -1,0 +1,100 @@
+"""Array-in, array-out entry points (drop-in for pkg/src/satsweep/api.py).
+
+``swa`` / ``multi_window`` keep the reference signatures and contracts: the
+caller's buffer is never mutated, results are freshly allocated (uint64 for
+integer sums, float64 otherwise), non-contiguous input is copied once, and
+errors use the reference's exception types.
+
+Placement follows the input: a numpy array goes through the C-ABI streaming
+path ``ssb_swa_host`` (host -> device -> host, banded and overlapped) and
+returns numpy; a CUDA ``torch.Tensor`` stays on the device and returns CUDA
+tensors.  Keyword-only extensions: ``pipeline`` ("auto" | "table" | "fused")
+and ``out`` (preallocated result array, e.g. in pinned memory).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _engine
+from .grid import ImageGrid, StatKind, WindowSpec, _is_torch
+
+METHODS = ("naive", "dp", "integral", "parallel")
+
+
+def _as_grid(array) -> ImageGrid:
+    if _is_torch(array):
+        if array.dim() != 2:
+            raise ValueError(f"expected a 2-D array, got {array.dim()} dimensions")
+        return ImageGrid.from_array(array) if array.is_cuda else _as_grid(array.numpy())
+    arr = np.asarray(array)
+    if arr.ndim != 2:
+        raise ValueError(f"expected a 2-D array, got {arr.ndim} dimensions")
+    # F32 finiteness is checked on the device by the first kernel that reads the
+    # raster (same GridValidationError), saving the reference's extra host pass.
+    return ImageGrid(np.ascontiguousarray(arr), _check_finite=False)
+
+
+def _check_method(method: str, threads: int) -> None:
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}; expected naive, dp, integral, or parallel")
+    if method == "parallel" and threads < 0:
+        raise ValueError(f"workers must be >= 0 (0 = auto), got {threads}")
+
+
+def swa_stats(array, window: int, stats=("sum",), stride: int = 1, *, pipeline: str = "auto", out=None) -> dict:
+    """Several statistics of one window from one pass (e.g. BASELINE C2's sum + mean).
+
+    Returns {stat name: array}."""
+    img = _as_grid(array)
+    win = WindowSpec(window, stride)
+    kinds = []
+    for s in stats:
+        k = StatKind.parse(s)
+        if k not in kinds:
+            kinds.append(k)
+    win.validate_for(img.rows, img.cols)
+    outs = None if out is None else {StatKind.parse(k): v for k, v in out.items()}
+    if img.on_device:
+        res = _engine.run_device(img, win.w, win.stride, kinds, pipeline, outs=outs)
+    else:
+        res = _engine.run_host(img, win.w, win.stride, kinds, pipeline, outs=outs)
+    return {k.value: res[k] for k in kinds}
+
+
+def swa(array, window: int, stat: str = "sum", method: str = "parallel", stride: int = 1, threads: int = 0, *,
+        pipeline: str = "auto", out=None):
+    """Sliding-window statistic over a 2-D array (api.py:28-55).
+
+    ``method`` is accepted for compatibility; every method runs the GPU path
+    (the reference guarantees all methods agree).  ``threads`` is ignored."""
+    img = _as_grid(array)
+    win = WindowSpec(window, stride)
+    kind = StatKind.parse(stat)
+    _check_method(method, threads)
+    win.validate_for(img.rows, img.cols)
+    outs = None if out is None else {kind: out}
+    if img.on_device:
+        return _engine.run_device(img, win.w, win.stride, [kind], pipeline, outs=outs)[kind]
+    return _engine.run_host(img, win.w, win.stride, [kind], pipeline, outs=outs)[kind]
+
+
+def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str = "table") -> list:
+    """Several window sizes from one set of tables (api.py:58-67); stride 1.
+
+    The default ``pipeline="table"`` builds the table(s) once, like the
+    reference; ``"fused"``/``"auto"`` may evaluate integer rasters without a
+    table (bit-identical results)."""
+    img = _as_grid(array)
+    specs = [WindowSpec(w) for w in windows]
+    kind = StatKind.parse(stat)
+    if not specs:
+        raise ValueError("windows list must be non-empty")
+    for s in specs:
+        s.validate_for(img.rows, img.cols)
+    from .integral import _run_tables
+
+    if pipeline == "table" or _engine.choose_pipeline(pipeline, img.elem_kind, max(windows), 1) == "table":
+        grid = img if img.on_device else ImageGrid(img.values, img.elem_kind, _check_finite=False)
+        return [r.values for r in _run_tables(grid, specs, kind)]
+    return [swa(array, s.w, kind.value, pipeline="fused") for s in specs]

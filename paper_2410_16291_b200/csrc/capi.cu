@@ -1,0 +1,350 @@
+// satsweep-b200: the extern "C" boundary (include/satsweep_b200.h).
+//
+// Validation mirrors the reference's error contract so the Python facade can
+// map status codes onto the same exception types:
+//   window/stride geometry  -> SSB_EINVAL  (InvalidWindowError, grid.py:133-143)
+//   allocation failure      -> SSB_ENOMEM  (ResourceLimitError, integral.py:76-83)
+//   non-finite F32 pixels   -> SSB_ENONFINITE (GridValidationError, grid.py:82-83)
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ssb_common.cuh"
+#include "../../include/satsweep_b200.h"
+
+#ifndef SSB_ENONFINITE
+#define SSB_ENONFINITE 5
+#endif
+
+namespace ssb {
+cudaError_t launch_sat_prepare(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, bool sq, void* ws,
+                               void* totals, void* totals_sq, int* nonfinite, cudaStream_t st);
+cudaError_t launch_sat_finish(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, void* sat_sq,
+                              int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, cudaStream_t st);
+int64_t sat_workspace_bytes(int dtype, int64_t R, int64_t C, bool sq);
+void sat_plan_info(int dtype, int64_t R, int64_t C, bool sq, int64_t* info);
+cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R, int64_t C,
+                               int64_t sat_ld, int64_t w, int64_t s, int mask, WinOut o, cudaStream_t st);
+cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
+                                WinOut o, int* nonfinite, int nK, cudaStream_t st);
+constexpr int64_t kFusedMaxWindow = 3072;
+
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace ssb
+
+using namespace ssb;
+
+namespace {
+thread_local std::string t_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) return fail(SSB_ENOMEM, "%s: %s", where, cudaGetErrorString(e));
+  return fail(SSB_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool valid_dtype(int d) { return d == SSB_U8 || d == SSB_U16 || d == SSB_I32 || d == SSB_F32; }
+int elem_size(int d) { return d == SSB_U8 ? 1 : d == SSB_U16 ? 2 : 4; }
+
+int check_image(int dtype, int64_t rows, int64_t cols, int64_t in_ld) {
+  if (!valid_dtype(dtype)) return fail(SSB_EUNSUPPORTED, "unsupported element dtype code %d", dtype);
+  if (rows < 1 || cols < 1) return fail(SSB_EINVAL, "grid dims must be >= 1, got %lldx%lld", (long long)rows, (long long)cols);
+  if (in_ld < cols) return fail(SSB_EINVAL, "in_ld %lld < cols %lld", (long long)in_ld, (long long)cols);
+  return SSB_OK;
+}
+
+int check_window(int64_t rows, int64_t cols, int64_t w, int64_t stride) {
+  if (w < 1) return fail(SSB_EINVAL, "window size must be >= 1, got %lld", (long long)w);
+  if (stride < 1) return fail(SSB_EINVAL, "stride must be >= 1, got %lld", (long long)stride);
+  if (w > rows || w > cols)
+    return fail(SSB_EINVAL, "window size %lld exceeds grid dims %lldx%lld; windows must fit fully inside the grid",
+                (long long)w, (long long)rows, (long long)cols);
+  return SSB_OK;
+}
+
+int check_stats(int dtype, int mask) {
+  if (mask == 0 || (mask & ~(SSB_SUM | SSB_MEAN | SSB_STD)) != 0) return fail(SSB_EINVAL, "bad stat mask %d", mask);
+  if (dtype == SSB_I32 && (mask & SSB_STD))
+    return fail(SSB_EUNSUPPORTED, "std is not supported for int32 input (squared sums exceed 64 bits)");
+  return SSB_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+int ssb_abi_version(void) { return SSB_ABI_VERSION; }
+const char* ssb_last_error(void) { return t_err.c_str(); }
+int64_t ssb_launch_count(void) { return (int64_t)g_launches.load(); }
+int64_t ssb_window_fused_max_w(void) { return kFusedMaxWindow; }
+
+int64_t ssb_sat_workspace_bytes(int in_dtype, int64_t rows, int64_t cols, int with_squares) {
+  if (!valid_dtype(in_dtype) || rows < 1 || cols < 1) return -1;
+  return sat_workspace_bytes(in_dtype, rows, cols, with_squares != 0);
+}
+
+int ssb_sat_plan(int in_dtype, int64_t rows, int64_t cols, int with_squares, int64_t* info4) {
+  if (!valid_dtype(in_dtype) || rows < 1 || cols < 1 || !info4) return fail(SSB_EINVAL, "bad plan request");
+  sat_plan_info(in_dtype, rows, cols, with_squares != 0, info4);
+  return SSB_OK;
+}
+
+int ssb_sat_prepare(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int with_squares,
+                    void* ws, int64_t ws_bytes, void* band_totals, void* band_totals_sq, int* nonfinite_flag,
+                    void* stream) {
+  int rc = check_image(in_dtype, rows, cols, in_ld);
+  if (rc) return rc;
+  if (in_dtype == SSB_I32 && with_squares) return fail(SSB_EUNSUPPORTED, "squared tables are not supported for int32 input");
+  const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, with_squares != 0);
+  if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  cudaError_t e = launch_sat_prepare(in_dtype, in, rows, cols, in_ld, with_squares != 0, ws, band_totals,
+                                     band_totals_sq, nonfinite_flag, as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_prepare");
+}
+
+int ssb_sat_finish(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat, void* sat_sq,
+                   int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, int64_t ws_bytes, void* stream) {
+  int rc = check_image(in_dtype, rows, cols, in_ld);
+  if (rc) return rc;
+  if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
+  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
+  if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
+    return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, sat_sq != nullptr);
+  if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  cudaError_t e = launch_sat_finish(in_dtype, in, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws,
+                                    as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_finish");
+}
+
+int ssb_sat_build(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat, void* sat_sq,
+                  int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, int64_t ws_bytes,
+                  int* nonfinite_flag, void* stream) {
+  int rc = ssb_sat_prepare(in, in_dtype, rows, cols, in_ld, sat_sq != nullptr, ws, ws_bytes, nullptr, nullptr,
+                           nonfinite_flag, stream);
+  if (rc) return rc;
+  return ssb_sat_finish(in, in_dtype, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws, ws_bytes, stream);
+}
+
+int ssb_window_eval(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols, int64_t sat_ld,
+                    int64_t w, int64_t stride, int stat_mask, void* out_sum, double* out_mean, double* out_std,
+                    int64_t out_ld, void* stream) {
+  int rc = check_image(in_dtype, rows, cols, cols);
+  if (rc) return rc;
+  if ((rc = check_window(rows, cols, w, stride))) return rc;
+  if ((rc = check_stats(in_dtype, stat_mask))) return rc;
+  if (!sat || sat_ld < cols + 1) return fail(SSB_EINVAL, "bad table");
+  if ((stat_mask & SSB_STD) && !sat_sq) return fail(SSB_EINVAL, "squared sums required for std dev");
+  if (((stat_mask & SSB_SUM) && !out_sum) || ((stat_mask & SSB_MEAN) && !out_mean) || ((stat_mask & SSB_STD) && !out_std))
+    return fail(SSB_EINVAL, "missing output buffer");
+  const int64_t out_c = (cols - w) / stride + 1;
+  if (out_ld < out_c) return fail(SSB_EINVAL, "out_ld < output cols");
+  WinOut o{out_sum, out_mean, out_std, out_ld};
+  cudaError_t e = launch_window_eval(sat, sat_sq, in_dtype == SSB_F32, in_dtype, rows, cols, sat_ld, w, stride,
+                                     stat_mask, o, as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_window_eval");
+}
+
+int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols,
+                          int64_t sat_ld, int n_windows, const int64_t* windows, int stat_mask,
+                          void* const* out_sums, double* const* out_means, double* const* out_stds,
+                          const int64_t* out_lds, void* stream) {
+  if (n_windows < 1 || !windows) return fail(SSB_EINVAL, "windows list must be non-empty");
+  for (int k = 0; k < n_windows; ++k) {  // validate all before any work (integral.py:205-208)
+    int rc = check_window(rows, cols, windows[k], 1);
+    if (rc) return rc;
+  }
+  for (int k = 0; k < n_windows; ++k) {
+    int rc = ssb_window_eval(sat, sat_sq, in_dtype, rows, cols, sat_ld, windows[k], 1, stat_mask,
+                             out_sums ? out_sums[k] : nullptr, out_means ? out_means[k] : nullptr,
+                             out_stds ? out_stds[k] : nullptr, out_lds[k], stream);
+    if (rc) return rc;
+  }
+  return SSB_OK;
+}
+
+int ssb_window_fused(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
+                     int stat_mask, void* out_sum, double* out_mean, double* out_std, int64_t out_ld,
+                     int* nonfinite_flag, int segments, void* stream) {
+  int rc = check_image(in_dtype, rows, cols, in_ld);
+  if (rc) return rc;
+  if ((rc = check_window(rows, cols, w, 1))) return rc;
+  if ((rc = check_stats(in_dtype, stat_mask))) return rc;
+  if (w > kFusedMaxWindow) return fail(SSB_EUNSUPPORTED, "fused path supports w <= %lld", (long long)kFusedMaxWindow);
+  if (((stat_mask & SSB_SUM) && !out_sum) || ((stat_mask & SSB_MEAN) && !out_mean) || ((stat_mask & SSB_STD) && !out_std))
+    return fail(SSB_EINVAL, "missing output buffer");
+  if (out_ld < cols - w + 1) return fail(SSB_EINVAL, "out_ld < output cols");
+  WinOut o{out_sum, out_mean, out_std, out_ld};
+  cudaError_t e = launch_window_fused(in, in_dtype, rows, cols, in_ld, w, stat_mask, o, nonfinite_flag, segments,
+                                      as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_window_fused");
+}
+
+int ssb_window_sum_at(const void* sat, int is_float_table, int64_t rows, int64_t cols, int64_t sat_ld, int64_t top,
+                      int64_t left, int64_t w, void* out_value, void* stream) {
+  if (w < 1 || top < 0 || left < 0 || top + w > rows || left + w > cols)  // integral.py:122-125
+    return fail(SSB_EINVAL, "%lldx%lld region at (%lld, %lld) does not lie within the %lldx%lld source", (long long)w,
+                (long long)w, (long long)top, (long long)left, (long long)rows, (long long)cols);
+  const uint64_t* t = reinterpret_cast<const uint64_t*>(sat);
+  uint64_t c[4];
+  const int64_t idx[4] = {(top + w) * sat_ld + left + w, top * sat_ld + left + w, (top + w) * sat_ld + left,
+                          top * sat_ld + left};
+  cudaStream_t st = as_stream(stream);
+  for (int k = 0; k < 4; ++k) {
+    cudaError_t e = cudaMemcpyAsync(&c[k], t + idx[k], 8, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "ssb_window_sum_at");
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "ssb_window_sum_at");
+  if (is_float_table) {
+    double d[4];
+    memcpy(d, c, sizeof(d));
+    const double v = (d[0] - d[1]) - (d[2] - d[3]);
+    memcpy(out_value, &v, 8);
+  } else {
+    const uint64_t v = (c[0] - c[1]) - (c[2] - c[3]);
+    memcpy(out_value, &v, 8);
+  }
+  return SSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer end-to-end path
+int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
+                 int64_t stride, int stat_mask, void* out_sum_host, double* out_mean_host, double* out_std_host,
+                 int64_t out_ld, int pipeline, int device, int64_t band_rows) {
+  int rc = check_image(in_dtype, rows, cols, in_ld);
+  if (rc) return rc;
+  if ((rc = check_window(rows, cols, w, stride))) return rc;
+  if ((rc = check_stats(in_dtype, stat_mask))) return rc;
+  if (pipeline == SSB_PIPE_FUSED && (stride != 1 || w > kFusedMaxWindow)) pipeline = SSB_PIPE_TABLE;
+  const bool sq = (stat_mask & SSB_STD) != 0;
+  const int es = elem_size(in_dtype);
+  const int64_t out_r = (rows - w) / stride + 1, out_c = (cols - w) / stride + 1;
+  if (out_ld < out_c) return fail(SSB_EINVAL, "out_ld < output cols");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+  // band geometry: output rows [o0, o1) need input rows [o0*s, (o1-1)*s + w)
+  const int64_t sat_ld = ((cols + 1) + 1) & ~int64_t(1);
+  const int nstats = ((stat_mask & SSB_SUM) ? 1 : 0) + ((stat_mask & SSB_MEAN) ? 1 : 0) + ((stat_mask & SSB_STD) ? 1 : 0);
+  auto in_rows_for = [&](int64_t nb) { return (nb - 1) * stride + w; };
+  if (band_rows <= 0) {
+    // ~6 GB of device buffers per band set, at least 4 bands when the image is large
+    const double per_out_row = (double)stride * ((double)cols * es +
+                               (pipeline == SSB_PIPE_TABLE ? 8.0 * sat_ld * (sq ? 2 : 1) : 0.0)) +
+                               8.0 * (double)out_c * nstats;
+    band_rows = (int64_t)(6.0e9 / per_out_row);
+    const int64_t quarter = (out_r + 3) / 4;
+    if (band_rows > quarter && out_r > 4096) band_rows = quarter;
+    if (band_rows < 1) band_rows = 1;
+  }
+  if (band_rows > out_r) band_rows = out_r;
+  const int64_t n_bands = (out_r + band_rows - 1) / band_rows;
+  const int n_sets = n_bands > 1 ? 2 : 1;
+  const int64_t max_in_rows = in_rows_for(band_rows);
+
+  const size_t in_bytes = (size_t)max_in_rows * cols * es;
+  const size_t sat_bytes = pipeline == SSB_PIPE_TABLE ? (size_t)(max_in_rows + 1) * sat_ld * 8 : 0;
+  const size_t ws_bytes = pipeline == SSB_PIPE_TABLE ? (size_t)sat_workspace_bytes(in_dtype, max_in_rows, cols, sq) : 0;
+  const size_t out_bytes = (size_t)band_rows * out_c * 8;
+
+  struct Set {
+    cudaStream_t st = nullptr;
+    void *in = nullptr, *sat = nullptr, *sq = nullptr, *ws = nullptr, *o_sum = nullptr, *o_mean = nullptr,
+         *o_std = nullptr;
+  };
+  std::vector<Set> sets(n_sets);
+  int* d_flag = nullptr;
+  int status = SSB_OK;
+  auto alloc = [&](void** p, size_t n, cudaStream_t st) -> bool {
+    if (n == 0) return true;
+    cudaError_t ae = cudaMallocAsync(p, n, st);
+    if (ae != cudaSuccess) { status = cuda_fail(ae, "device allocation"); return false; }
+    return true;
+  };
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed blocks cached across calls
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  for (auto& s : sets) {
+    if ((e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking)) != cudaSuccess) { status = cuda_fail(e, "stream"); break; }
+    if (!alloc(&s.in, in_bytes, s.st) || !alloc(&s.sat, sat_bytes, s.st) || !alloc(&s.sq, sq ? sat_bytes : 0, s.st) ||
+        !alloc(&s.ws, ws_bytes, s.st) || !alloc(&s.o_sum, (stat_mask & SSB_SUM) ? out_bytes : 0, s.st) ||
+        !alloc(&s.o_mean, (stat_mask & SSB_MEAN) ? out_bytes : 0, s.st) ||
+        !alloc(&s.o_std, (stat_mask & SSB_STD) ? out_bytes : 0, s.st))
+      break;
+  }
+  if (status == SSB_OK && (e = cudaMalloc(&d_flag, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
+  if (status == SSB_OK && (e = cudaMemset(d_flag, 0, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
+
+  for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
+    Set& s = sets[b % n_sets];
+    const int64_t o0 = b * band_rows, o1 = (o0 + band_rows < out_r) ? o0 + band_rows : out_r;
+    const int64_t nb = o1 - o0, r0 = o0 * stride, nr = in_rows_for(nb);
+    const char* src = reinterpret_cast<const char*>(in_host) + (size_t)r0 * in_ld * es;
+    if ((e = cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es, (size_t)nr,
+                               cudaMemcpyHostToDevice, s.st)) != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
+    WinOut o{s.o_sum, reinterpret_cast<double*>(s.o_mean), reinterpret_cast<double*>(s.o_std), out_c};
+    if (pipeline == SSB_PIPE_TABLE) {
+      e = launch_sat_prepare(in_dtype, s.in, nr, cols, cols, sq, s.ws, nullptr, nullptr, d_flag, s.st);
+      if (e == cudaSuccess)
+        e = launch_sat_finish(in_dtype, s.in, nr, cols, cols, s.sat, s.sq, sat_ld, nullptr, nullptr, s.ws, s.st);
+      if (e == cudaSuccess)
+        e = launch_window_eval(s.sat, s.sq, in_dtype == SSB_F32, in_dtype, nr, cols, sat_ld, w, stride, stat_mask, o, s.st);
+    } else {
+      e = launch_window_fused(s.in, in_dtype, nr, cols, cols, w, stat_mask, o, d_flag, 0, s.st);
+    }
+    if (e != cudaSuccess) { status = cuda_fail(e, "band compute"); break; }
+    auto d2h = [&](void* host, void* dev) -> bool {
+      if (!host) return true;
+      char* dst = reinterpret_cast<char*>(host) + (size_t)o0 * out_ld * 8;
+      cudaError_t ce = cudaMemcpy2DAsync(dst, (size_t)out_ld * 8, dev, (size_t)out_c * 8, (size_t)out_c * 8,
+                                         (size_t)nb, cudaMemcpyDeviceToHost, s.st);
+      if (ce != cudaSuccess) { status = cuda_fail(ce, "D2H"); return false; }
+      return true;
+    };
+    if (!d2h((stat_mask & SSB_SUM) ? out_sum_host : nullptr, s.o_sum) ||
+        !d2h((stat_mask & SSB_MEAN) ? out_mean_host : nullptr, s.o_mean) ||
+        !d2h((stat_mask & SSB_STD) ? out_std_host : nullptr, s.o_std))
+      break;
+  }
+  for (auto& s : sets) {
+    if (!s.st) continue;
+    cudaError_t se = cudaStreamSynchronize(s.st);
+    if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");
+    void* ptrs[] = {s.in, s.sat, s.sq, s.ws, s.o_sum, s.o_mean, s.o_std};
+    for (void* p : ptrs) if (p) cudaFreeAsync(p, s.st);
+    cudaStreamSynchronize(s.st);
+    cudaStreamDestroy(s.st);
+  }
+  if (d_flag) {
+    int h = 0;
+    if (status == SSB_OK) {
+      cudaError_t fe = cudaMemcpy(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost);
+      if (fe != cudaSuccess) status = cuda_fail(fe, "flag D2H");
+    }
+    cudaFree(d_flag);
+    if (status == SSB_OK && h) status = fail(SSB_ENONFINITE, "F32 grid contains NaN or Inf; only finite values are admitted");
+  }
+  return status;
+}
+
+}  // extern "C"

@@ -1,0 +1,298 @@
+// satsweep-b200: fused window statistics that never materialise the table.
+//
+// Same outputs as build_sat + sweep_window_sums + finalize
+// (pkg/src/satsweep/integral.py:109-116, :141-163; stats.py:35-74) for stride 1,
+// computed from the image directly.  The four-corner identity needs only
+// *local* prefix sums: a per-column offset added to every table row cancels in
+// (br - tr) and a per-row offset cancels in (bl - tl).  Each CTA
+// owns a strip of output columns and a segment of output rows and keeps, per
+// image column of the strip (+ w-1 halo columns), the vertical running sum of
+// the last w rows in registers:
+//     V[c] += x[r][c] - x[r-w][c]
+// Each finished row is prefix-summed across the strip (warp shuffles + one
+// cross-warp step) and out[j] = P[j+w] - P[j].  Row x[r-w] is re-read from L2.
+//
+// Integer sums use modular arithmetic of the narrowest width that holds the
+// final window sum (u32 for u8 while w^2*255 < 2^32), so intermediate prefix
+// sums may wrap without affecting the result.  f32 input uses double.
+#include "ssb_common.cuh"
+
+namespace ssb {
+
+template <typename InT, int E>
+__device__ __forceinline__ void load_cols(const InT* __restrict__ p, int64_t c0, int64_t C, bool vec_ok, InT (&x)[E]) {
+  constexpr int kBytes = E * (int)sizeof(InT);
+  if (vec_ok && c0 + E <= C) {
+    if constexpr (kBytes == 4) {
+      const uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(p + c0));
+      memcpy(x, &v, 4);
+    } else if constexpr (kBytes == 8) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p + c0));
+      memcpy(x, &v, 8);
+    } else {
+      static_assert(kBytes % 16 == 0, "vector width");
+#pragma unroll
+      for (int k = 0; k < kBytes / 16; ++k) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + c0) + k);
+        memcpy(reinterpret_cast<char*>(x) + 16 * k, &v, 16);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = (c0 + k < C) ? __ldg(p + c0 + k) : InT(0);
+  }
+}
+
+template <typename VT> __device__ __forceinline__ VT tv(uint8_t x) { return (VT)x; }
+template <typename VT> __device__ __forceinline__ VT tv(uint16_t x) { return (VT)x; }
+template <typename VT> __device__ __forceinline__ VT tv(int32_t x) { return (VT)(int64_t)x; }
+template <typename VT> __device__ __forceinline__ VT tv(float x) { return (VT)x; }
+
+struct FusedGeom {
+  int64_t R, C, in_ld, out_r, out_c;
+  int w;
+  int two;      // output columns per strip
+  int64_t sro;  // output rows per segment
+  int mask;
+  int vec_ok;
+};
+
+template <typename InT, typename VT, typename VQ, bool SQ, int E, int G>
+struct FusedSmem {
+  static constexpr int NV = kThreads * E;
+  VT p[G][NV + 1];
+  VQ pq[SQ ? G : 1][SQ ? NV + 1 : 1];
+  VT sw[G][kThreads / 32];
+  VQ swq[G][kThreads / 32];
+};
+
+template <typename InT, typename VT, typename VQ, bool SQ, int E, int G>
+__global__ void __launch_bounds__(kThreads)
+window_fused_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeInt fi, int* __restrict__ nonfinite) {
+  using SM = FusedSmem<InT, VT, VQ, SQ, E, G>;
+  constexpr bool kFloat = Elem<InT>::kFloat;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t oc0 = (int64_t)blockIdx.x * g.two;
+  const int64_t or0 = (int64_t)blockIdx.y * g.sro;
+  const int64_t or1 = min(or0 + g.sro, g.out_r);
+  const int nout = (int)((g.out_c - oc0) < g.two ? (g.out_c - oc0) : g.two);
+  if (or0 >= or1 || nout <= 0) return;
+  const int w = g.w;
+  const int64_t c0 = oc0 + (int64_t)tid * E;  // first image column owned
+  const int64_t r_end = or1 + w - 1;          // one past last input row
+  int nf = 0;
+
+  VT V[E];
+  VQ Vq[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) { V[k] = VT(0); Vq[k] = VQ(0); }
+
+  for (int64_t rb = or0; rb < r_end; rb += G) {
+    VT S[G][E];
+    VQ Q[G][E];
+    // ---- vertical sliding update for G rows
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      const int64_t r = rb + gg;
+      if (r < r_end) {
+        InT xn[E];
+        load_cols<InT, E>(in + r * g.in_ld, c0, g.C, g.vec_ok, xn);
+        if (r - w >= or0) {
+          InT xo[E];
+          load_cols<InT, E>(in + (r - w) * g.in_ld, c0, g.C, g.vec_ok, xo);
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            V[k] = sub(add(V[k], tv<VT>(xn[k])), tv<VT>(xo[k]));
+            if constexpr (SQ) {
+              if constexpr (kFloat) Vq[k] = sub(add(Vq[k], __dmul_rn((double)xn[k], (double)xn[k])), __dmul_rn((double)xo[k], (double)xo[k]));
+              else Vq[k] = sub(add(Vq[k], tv<VQ>(xn[k]) * tv<VQ>(xn[k])), tv<VQ>(xo[k]) * tv<VQ>(xo[k]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            V[k] = add(V[k], tv<VT>(xn[k]));
+            if constexpr (SQ) {
+              if constexpr (kFloat) Vq[k] = add(Vq[k], __dmul_rn((double)xn[k], (double)xn[k]));
+              else Vq[k] = add(Vq[k], tv<VQ>(xn[k]) * tv<VQ>(xn[k]));
+            }
+          }
+        }
+        if constexpr (kFloat) {
+#pragma unroll
+          for (int k = 0; k < E; ++k) if (is_nonfinite(xn[k])) nf = 1;
+        }
+      }
+      // inclusive prefix inside the thread's E columns
+      VT run = VT(0);
+      VQ runq = VQ(0);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        run = add(run, V[k]); S[gg][k] = run;
+        if constexpr (SQ) { runq = add(runq, Vq[k]); Q[gg][k] = runq; }
+      }
+      // warp scan of thread totals
+      const VT inc = warp_incl_scan(run, lane);
+      const VT exc = sub(inc, run);
+#pragma unroll
+      for (int k = 0; k < E; ++k) S[gg][k] = add(S[gg][k], exc);
+      if (lane == 31) sm.sw[gg][warp] = inc;
+      if constexpr (SQ) {
+        const VQ incq = warp_incl_scan(runq, lane);
+        const VQ excq = sub(incq, runq);
+#pragma unroll
+        for (int k = 0; k < E; ++k) Q[gg][k] = add(Q[gg][k], excq);
+        if (lane == 31) sm.swq[gg][warp] = incq;
+      }
+    }
+    __syncthreads();
+    // ---- cross-warp offsets, publish P rows: P[m] = sum_{c<m} V[c]
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      VT off = VT(0);
+      VQ offq = VQ(0);
+      for (int w2 = 0; w2 < warp; ++w2) {
+        off = add(off, sm.sw[gg][w2]);
+        if constexpr (SQ) offq = add(offq, sm.swq[gg][w2]);
+      }
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        sm.p[gg][tid * E + k + 1] = add(off, S[gg][k]);
+        if constexpr (SQ) sm.pq[gg][tid * E + k + 1] = add(offq, Q[gg][k]);
+      }
+      if (tid == 0) {
+        sm.p[gg][0] = VT(0);
+        if constexpr (SQ) sm.pq[gg][0] = VQ(0);
+      }
+    }
+    __syncthreads();
+    // ---- outputs for the rows of this group that complete a window
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      const int64_t r = rb + gg;
+      const int64_t i = r - (w - 1);
+      if (r < r_end && i >= or0) {
+        const int64_t base = i * o.ld + oc0;
+        for (int j = tid; j < nout; j += kThreads) {
+          const VT sv = sub(sm.p[gg][j + w], sm.p[gg][j]);
+          VQ qv = VQ(0);
+          if constexpr (SQ) qv = sub(sm.pq[gg][j + w], sm.pq[gg][j]);
+          if constexpr (kFloat) {
+            if (g.mask & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + base + j, (double)sv);
+            if (g.mask & ST_MEAN) st_cs(o.mean + base + j, fin_mean_f((double)sv, fi.dn));
+            if (g.mask & ST_STD) st_cs(o.std_ + base + j, fin_std_f((double)sv, (double)qv, fi.dn));
+          } else {
+            // widen modular result: unsigned for u8/u16, sign-extended for i32
+            uint64_t s64;
+            if constexpr (sizeof(VT) == 4) s64 = (uint64_t)(uint32_t)sv;
+            else s64 = (uint64_t)sv;
+            uint64_t q64 = 0;
+            if constexpr (SQ) {
+              if constexpr (sizeof(VQ) == 4) q64 = (uint64_t)(uint32_t)qv;
+              else q64 = (uint64_t)qv;
+            }
+            if (g.mask & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + base + j, s64);
+            if (g.mask & ST_MEAN) st_cs(o.mean + base + j, fin_mean_int(s64, fi));
+            if (g.mask & ST_STD) st_cs(o.std_ + base + j, fin_std_int(s64, q64, fi));
+          }
+        }
+      }
+    }
+    // the next group's first __syncthreads protects sm.p / sm.sw reuse
+  }
+  if (nf && nonfinite) atomicOr(nonfinite, 1);
+}
+
+template <typename InT, typename VT, typename VQ, bool SQ, int E, int G>
+cudaError_t launch_fused_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK_override,
+                           cudaStream_t st) {
+  using SM = FusedSmem<InT, VT, VQ, SQ, E, G>;
+  constexpr int NV = SM::NV;
+  int two = NV - g.w + 1;
+  two = (two / 16) * 16;
+  if (two < 16) return cudaErrorInvalidValue;
+  g.two = two;
+  const int64_t nJ = (g.out_c + two - 1) / two;
+  int64_t nK = nK_override > 0 ? nK_override : (2 * kNumSMs + nJ - 1) / nJ;
+  if (nK > g.out_r) nK = g.out_r;
+  if (nK < 1) nK = 1;
+  g.sro = (g.out_r + nK - 1) / nK;
+  nK = (g.out_r + g.sro - 1) / g.sro;
+  auto kfn = window_fused_kernel<InT, VT, VQ, SQ, E, G>;
+  const size_t smem = sizeof(SM);
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)nJ, (unsigned)nK);
+  kfn<<<grid, kThreads, smem, st>>>(reinterpret_cast<const InT*>(in), g, o, fi, nonfinite);
+  note_launch(1);
+  return cudaGetLastError();
+}
+
+// rows per group: keep the G x E snapshot registers at <= 64 32-bit registers
+template <typename VT, typename VQ, bool SQ, int E>
+constexpr int fused_group() {
+  constexpr int words = E * ((int)sizeof(VT) + (SQ ? (int)sizeof(VQ) : 0)) / 4;
+  constexpr int g = 64 / words;
+  return g >= 8 ? 8 : g >= 4 ? 4 : g >= 2 ? 2 : 1;
+}
+
+template <typename InT, typename VT, typename VQ, bool SQ>
+cudaError_t launch_fused_e(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK, cudaStream_t st) {
+  if (g.w <= 256) return launch_fused_t<InT, VT, VQ, SQ, 4, fused_group<VT, VQ, SQ, 4>()>(in, g, o, fi, nonfinite, nK, st);
+  if (g.w <= 1024) return launch_fused_t<InT, VT, VQ, SQ, 8, fused_group<VT, VQ, SQ, 8>()>(in, g, o, fi, nonfinite, nK, st);
+  return launch_fused_t<InT, VT, VQ, SQ, 16, fused_group<VT, VQ, SQ, 16>()>(in, g, o, fi, nonfinite, nK, st);
+}
+
+// Largest window the fused path accepts (wider windows go through the table).
+constexpr int kFusedMaxW = 3072;
+
+cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
+                                WinOut o, int* nonfinite, int nK, cudaStream_t st) {
+  if (w < 1 || w > kFusedMaxW) return cudaErrorInvalidValue;
+  FusedGeom g{};
+  g.R = R; g.C = C; g.in_ld = in_ld; g.w = (int)w; g.mask = mask;
+  g.out_r = R - w + 1; g.out_c = C - w + 1;
+  const int es = dtype == IN_U8 ? 1 : dtype == IN_U16 ? 2 : 4;
+  const int E = w <= 256 ? 4 : w <= 1024 ? 8 : 16;
+  int vb = E * es; if (vb > 16) vb = 16;
+  g.vec_ok = ((reinterpret_cast<uintptr_t>(in) % vb) == 0) && (((in_ld * es) % vb) == 0);
+  const bool sq = (mask & ST_STD) != 0;
+  FinalizeInt fi{};
+  fi.n = (uint64_t)(w * w);
+  fi.dn = (double)(w * w);
+  const double maxv = dtype == IN_U8 ? 255.0 : dtype == IN_U16 ? 65535.0 : 2147483648.0;
+  fi.u64_ok = ((unsigned __int128)(uint64_t)(w * w) * (uint64_t)maxv) <= (unsigned __int128)0xFFFFFFFFull;
+  fi.is_signed = dtype == IN_I32;
+  const unsigned __int128 ww = (unsigned __int128)(uint64_t)(w * w);
+  switch (dtype) {
+    case IN_U8: {
+      const bool s32 = ww * 255u < ((unsigned __int128)1 << 32);
+      const bool q32 = ww * 65025u < ((unsigned __int128)1 << 32);
+      if (!sq) return s32 ? launch_fused_e<uint8_t, uint32_t, uint32_t, false>(in, g, o, fi, nonfinite, nK, st)
+                          : launch_fused_e<uint8_t, uint64_t, uint64_t, false>(in, g, o, fi, nonfinite, nK, st);
+      if (s32 && q32) return launch_fused_e<uint8_t, uint32_t, uint32_t, true>(in, g, o, fi, nonfinite, nK, st);
+      if (s32) return launch_fused_e<uint8_t, uint32_t, uint64_t, true>(in, g, o, fi, nonfinite, nK, st);
+      return launch_fused_e<uint8_t, uint64_t, uint64_t, true>(in, g, o, fi, nonfinite, nK, st);
+    }
+    case IN_U16: {
+      const bool s32 = ww * 65535u < ((unsigned __int128)1 << 32);
+      if (!sq) return s32 ? launch_fused_e<uint16_t, uint32_t, uint64_t, false>(in, g, o, fi, nonfinite, nK, st)
+                          : launch_fused_e<uint16_t, uint64_t, uint64_t, false>(in, g, o, fi, nonfinite, nK, st);
+      return s32 ? launch_fused_e<uint16_t, uint32_t, uint64_t, true>(in, g, o, fi, nonfinite, nK, st)
+                 : launch_fused_e<uint16_t, uint64_t, uint64_t, true>(in, g, o, fi, nonfinite, nK, st);
+    }
+    case IN_I32:
+      if (sq) return cudaErrorInvalidValue;
+      return launch_fused_e<int32_t, uint64_t, uint64_t, false>(in, g, o, fi, nonfinite, nK, st);
+    case IN_F32:
+      return sq ? launch_fused_e<float, double, double, true>(in, g, o, fi, nonfinite, nK, st)
+                : launch_fused_e<float, double, double, false>(in, g, o, fi, nonfinite, nK, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ssb

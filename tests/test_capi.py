@@ -1,0 +1,61 @@
+"""The C-ABI shared library loads and exports every symbol include/satsweep_b200.h
+declares; argument validation works without a GPU (no compute calls here)."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+
+import pytest
+
+from conftest import REPO
+from paper_2410_16291_b200 import _lib, build_ext
+
+HEADER = REPO / "include" / "satsweep_b200.h"
+
+
+def declared_symbols() -> list[str]:
+    return sorted(set(re.findall(r"\b(ssb_\w+)\s*\(", HEADER.read_text())))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build_ext.build()
+    return _lib.load()
+
+
+def test_header_and_binding_agree():
+    assert sorted(_lib.EXPORTS) == declared_symbols()
+
+
+def test_every_symbol_exported(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_abi_version(lib):
+    assert lib.ssb_abi_version() == 1
+
+
+def test_workspace_and_plan(lib):
+    ws = lib.ssb_sat_workspace_bytes(_lib.U8, 70000, 85000, 0)
+    assert 0 < ws < 512 * 2**20  # carry vectors are ~1/50 of the table
+    info = (ctypes.c_int64 * 4)()
+    assert lib.ssb_sat_plan(_lib.U8, 70000, 85000, 0, info) == 0
+    tw, sr, nj, nk = list(info)
+    assert tw == 512 and nj * tw >= 85001 and nk * sr >= 70001
+    assert lib.ssb_sat_workspace_bytes(99, 10, 10, 0) == -1
+
+
+def test_validation_without_device(lib):
+    # window larger than the grid: rejected before any CUDA call
+    rc = lib.ssb_window_eval(None, None, _lib.U8, 4, 4, 6, 5, 1, _lib.SUM, None, None, None, 1, None)
+    assert rc == _lib.EINVAL and b"exceeds grid dims" in lib.ssb_last_error()
+    rc = lib.ssb_window_fused(None, _lib.I32, 8, 8, 8, 3, _lib.STD, None, None, None, 6, None, 0, None)
+    assert rc == _lib.EUNSUPPORTED
+    rc = lib.ssb_window_sum_at(None, 0, 4, 4, 6, 3, 0, 2, None, None)
+    assert rc == _lib.EINVAL and b"does not lie within" in lib.ssb_last_error()
+    rc = lib.ssb_window_eval_multi(None, None, _lib.U8, 8, 8, 10, 0, None, _lib.SUM, None, None, None, None, None)
+    assert rc == _lib.EINVAL
+    with pytest.raises(_lib.InvalidWindowError):
+        _lib.check(lib.ssb_window_eval(None, None, _lib.U8, 4, 4, 6, 0, 1, _lib.SUM, None, None, None, 1, None))

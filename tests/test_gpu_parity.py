@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Integer results bit-exact; F32 within rtol 1e-6
+plus the reference's derived atol floor (conftest.assert_matches)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import assert_matches, digest, random_values
+from oracle import satsweep_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("u8", "u16", "f32")
+PIPES = ("table", "fused")
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2410_16291_b200 import _lib, build_ext
+
+    build_ext.build()
+    _lib.load()
+    import paper_2410_16291_b200 as mod
+
+    return mod
+
+
+def to_dev(a):
+    import torch
+
+    from paper_2410_16291_b200 import _device
+
+    return _device.to_device(a, torch.device("cuda", 0))
+
+
+def host(t, dtype):
+    from paper_2410_16291_b200 import _device
+
+    return _device.to_host(t, dtype)
+
+
+# ---------------------------------------------------------------- tables
+def test_hand_tables(sb, golden):
+    img = sb.ImageGrid(golden["hand_in"])
+    sat = sb.build_sat(img)
+    assert sat.table.tolist() == [[0, 0, 0], [0, 1, 3], [0, 4, 10]]
+    assert sat.accum_kind is sb.AccumKind.U64 and sat.source_dims == (2, 2)
+    assert sb.build_sat(img, squared=True).table.tolist() == [[0, 0, 0], [0, 1, 5], [0, 10, 30]]
+    assert sb.build_sat(sb.ImageGrid(np.zeros((4, 5), np.uint16))).table.tolist() == np.zeros((5, 6), int).tolist()
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("sq", [False, True])
+def test_random_tables(sb, golden, kind, sq):
+    v = golden[f"rand_{kind}_in"]
+    ref = golden[f"rand_{kind}_sat{'_sq' if sq else ''}"]
+    got = sb.build_sat(sb.ImageGrid(v), squared=sq).table
+    if kind == "f32":
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-9)
+    else:
+        np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 700), (700, 1), (33, 513), (513, 33), (1025, 1537), (3000, 2049)])
+@pytest.mark.parametrize("kind", ["u8", "u16", "i32", "f32"])
+def test_tables_vs_oracle_shapes(sb, shape, kind):
+    rng = np.random.default_rng(hash((shape, kind)) % 2**32)
+    if kind == "i32":
+        v = rng.integers(-(2**31), 2**31, size=shape, dtype=np.int64).astype(np.int32)
+    else:
+        v = random_values(rng, *shape, kind)
+    for sq in (False, True) if kind != "i32" else (False,):
+        got = sb.build_sat(sb.ImageGrid(v), squared=sq).table
+        ref = O.build_table(v, sq)
+        if kind == "f32":
+            np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-9 * max(1, shape[0] * shape[1]))
+        elif ref.dtype == object:
+            assert got.tolist() == ref.tolist()
+        else:
+            np.testing.assert_array_equal(got.view(ref.dtype), ref)
+
+
+def test_zero_border_and_monotone(sb, rng):
+    for kind in KINDS:
+        v = random_values(rng, 31, 12, kind)
+        for sq in (False, True):
+            t = np.asarray(sb.build_sat(sb.ImageGrid(v), squared=sq).table, dtype=np.float64)
+            assert (t[0] == 0).all() and (t[:, 0] == 0).all()
+            assert (np.diff(t, axis=0) >= 0).all() and (np.diff(t, axis=1) >= 0).all()
+
+
+def test_window_sum(sb, golden, rng):
+    sat = sb.build_sat(sb.ImageGrid(golden["hand_in"]))
+    assert sb.window_sum(sat, 0, 0, 2) == 10 and sb.window_sum(sat, 0, 1, 1) == 2
+    for top, left, w in [(1, 0, 2), (0, 1, 2), (-1, 0, 1), (0, -1, 1), (0, 0, 3)]:
+        with pytest.raises(sb.InvalidWindowError):
+            sb.window_sum(sat, top, left, w)
+    arr = rng.integers(0, 65536, size=(20, 20), dtype=np.uint16)
+    s = sb.build_sat(sb.ImageGrid(arr))
+    q = sb.build_sat(sb.ImageGrid(arr), squared=True)
+    for top, left, w in [(0, 0, 20), (3, 5, 7), (12, 0, 8), (19, 19, 1)]:
+        assert int(sb.window_sum(s, top, left, w)) == int(arr[top:top + w, left:left + w].astype(np.uint64).sum())
+    for i in range(6):
+        for j in range(7):
+            assert sb.window_sum(q, i, j, 1) == int(arr[i, j]) ** 2
+
+
+# ---------------------------------------------------------------- window statistics
+@pytest.mark.parametrize("kind", KINDS)
+def test_swa_golden_cases(sb, golden, kind):
+    for ci, (r, c, w, s) in enumerate(golden["cases"].tolist()):
+        v = golden[f"case{ci}_{kind}_in"]
+        img = sb.ImageGrid(v)
+        for stat in ("sum", "mean", "std"):
+            ref = golden[f"case{ci}_{kind}_{stat}"]
+            got = sb.swa_integral(img, sb.WindowSpec(w, s), sb.StatKind(stat)).values
+            assert got.dtype == ref.dtype
+            assert_matches(got, ref, v, stat, w)
+            if s == 1:
+                fused = sb.swa(v, w, stat, pipeline="fused")
+                assert_matches(fused, ref, v, stat, w)
+
+
+def test_wide_numerator_std(sb, golden):
+    v = golden["wide_u16_in"]
+    for pipe in PIPES:
+        got = sb.swa(v, 300, "std", pipeline=pipe)
+        np.testing.assert_array_equal(got, golden["wide_u16_std"])
+
+
+def test_std_examples(sb):
+    assert sb.swa(np.array([[0, 2], [0, 2]], np.uint8), 2, "std").tolist() == [[1.0]]
+    arr = np.full((12, 12), 9, dtype=np.uint16)
+    for w in (1, 3, 5):
+        for pipe in PIPES:
+            np.testing.assert_array_equal(sb.swa(arr, w, "std", pipeline=pipe), np.zeros((12 - w + 1,) * 2))
+
+
+def test_multi_window(sb, golden):
+    v = golden["mw_in"]
+    for stat in ("sum", "mean", "std"):
+        for w, got in zip((5, 50, 150), sb.multi_window(v, [5, 50, 150], stat)):
+            np.testing.assert_array_equal(got, golden[f"mw_{stat}_{w}"])
+    a, b = sb.multi_window(v, [7, 7], "sum")
+    np.testing.assert_array_equal(a, b)
+
+
+def test_acceptance_sweep(sb, hashes):
+    """210 seeded images x 3 stats x 2 pipelines (pkg/tests/test_acceptance.py:37-74)."""
+    rng = np.random.default_rng(20240817)
+    for rec in hashes["acceptance"]:
+        rows, cols = int(rng.integers(rec["w"], 257)), int(rng.integers(rec["w"], 257))
+        assert (rows, cols) == (rec["rows"], rec["cols"])
+        v = random_values(rng, rows, cols, rec["kind"])
+        w, s = rec["w"], rec["stride"]
+        for stat in ("sum", "mean", "std"):
+            got = sb.swa(v, w, stat, stride=s, pipeline="table")
+            if rec["kind"] == "f32":
+                assert_matches(got, O.swa(v, w, stat, s), v, stat, w)
+            else:
+                assert digest(got) == rec[stat], rec
+            if s == 1:
+                fz = sb.swa(v, w, stat, pipeline="fused")
+                if rec["kind"] == "f32":
+                    assert_matches(fz, O.swa(v, w, stat, s), v, stat, w)
+                else:
+                    assert digest(fz) == rec[stat], rec
+
+
+@pytest.mark.parametrize("pipe", PIPES)
+def test_random_shapes_vs_oracle(sb, pipe):
+    rng = np.random.default_rng(7777)
+    for _ in range(40):
+        kind = KINDS[int(rng.integers(0, 3))]
+        rows, cols = int(rng.integers(1, 700)), int(rng.integers(1, 2200))
+        w = int(rng.integers(1, min(rows, cols) + 1))
+        v = random_values(rng, rows, cols, kind)
+        for stat in ("sum", "mean", "std"):
+            got = sb.swa(v, w, stat, pipeline=pipe)
+            assert_matches(got, O.swa(v, w, stat), v, stat, w)
+
+
+def test_int32_extension(sb):
+    rng = np.random.default_rng(2)
+    v = rng.integers(-(2**31), 2**31, size=(300, 400), dtype=np.int64).astype(np.int32)
+    for pipe in PIPES:
+        for stat in ("sum", "mean"):
+            got = sb.swa(v, 17, stat, pipeline=pipe)
+            ref = O.swa(v, 17, stat)
+            assert got.dtype == ref.dtype
+            np.testing.assert_array_equal(got, ref)
+    with pytest.raises(TypeError):
+        sb.swa(v, 3, "std")
+
+
+def test_device_tensor_in_device_tensor_out(sb):
+    rng = np.random.default_rng(9)
+    v = random_values(rng, 257, 300, "u16")
+    d = to_dev(v)
+    for pipe in PIPES:
+        out = sb.swa(d, 31, "mean", pipeline=pipe)
+        assert out.is_cuda
+        np.testing.assert_array_equal(host(out, np.float64), O.swa(v, 31, "mean"))
+    res = sb.swa_stats(d, 31, ("sum", "mean", "std"))
+    np.testing.assert_array_equal(host(res["sum"], np.uint64), O.swa(v, 31, "sum"))
+    np.testing.assert_array_equal(host(res["std"], np.float64), O.swa(v, 31, "std"))
+
+
+# ---------------------------------------------------------------- API contract
+def test_api_contract(sb):
+    import hashlib
+
+    rng = np.random.default_rng(13)
+    arr = rng.integers(0, 65536, size=(50, 50), dtype=np.uint16)
+    before = hashlib.sha256(arr.tobytes()).hexdigest()
+    for method in ("naive", "dp", "integral", "parallel"):
+        sb.swa(arr, 7, "std", method)
+    assert hashlib.sha256(arr.tobytes()).hexdigest() == before
+    big = rng.integers(0, 256, size=(20, 40), dtype=np.uint8)
+    view = big[:, ::2]
+    np.testing.assert_array_equal(sb.swa(view, 3, "sum", "integral"), sb.swa(np.ascontiguousarray(view), 3))
+    ones = np.ones((4, 4), dtype=np.uint8)
+    out = sb.swa(ones, 1, "sum")
+    assert out.dtype == np.uint64 and (out.base is None or out.base is not ones)
+    out[0, 0] = 99
+    assert ones[0, 0] == 1
+    arr = rng.integers(0, 65536, size=(33, 29), dtype=np.uint16)
+    res = [sb.swa(arr, 5, "sum", m, stride=2) for m in ("naive", "dp", "integral", "parallel")]
+    for r in res[1:]:
+        np.testing.assert_array_equal(res[0], r)
+
+
+def test_nonfinite_rejected(sb):
+    bad = np.ones((16, 16), dtype=np.float32)
+    bad[3, 4] = np.nan
+    for pipe in PIPES:
+        with pytest.raises(sb.GridValidationError):
+            sb.swa(bad, 3, "mean", pipeline=pipe)
+    bad[3, 4] = np.inf
+    with pytest.raises(sb.GridValidationError):
+        sb.swa_stats(to_dev(bad), 3, ("sum",), pipeline="table")
+
+
+def test_parallel_census_and_identity(sb, rng):
+    census = sb.WriteCensus()
+    v = random_values(rng, 41, 29, "u16")
+    win = sb.WindowSpec(7, 2)
+    cfg = sb.ParallelConfig(workers=4, min_parallel_elems=1, census=census)
+    par = sb.swa_parallel(sb.ImageGrid(v), win, sb.StatKind.STD, cfg)
+    np.testing.assert_array_equal(par.values, sb.swa_integral(sb.ImageGrid(v), win, sb.StatKind.STD).values)
+    out_r, _ = sb.output_dims(41, 29, win)
+    for phase, total in [("rows/sum", 41), ("cols/sum", 29), ("rows/sq", 41), ("cols/sq", 29),
+                         ("query/sum", out_r), ("query/sq", out_r)]:
+        census.assert_disjoint_cover(phase, total)
+
+
+def test_host_streaming_bands(sb):
+    """ssb_swa_host with several bands equals one-shot evaluation (offsets cancel per band)."""
+    from paper_2410_16291_b200 import _engine
+
+    rng = np.random.default_rng(21)
+    for kind in KINDS:
+        v = random_values(rng, 611, 333, kind)
+        img = sb.ImageGrid(v)
+        for pipe in PIPES:
+            for stride in (1, 3) if pipe == "table" else (1,):
+                one = _engine.run_host(img, 40, stride, [sb.StatKind.SUM, sb.StatKind.STD], pipe)
+                many = _engine.run_host(img, 40, stride, [sb.StatKind.SUM, sb.StatKind.STD], pipe, band_rows=37)
+                for k in one:
+                    if kind == "f32":
+                        np.testing.assert_allclose(many[k], one[k], rtol=1e-9, atol=1e-9)
+                    else:
+                        np.testing.assert_array_equal(many[k], one[k])
