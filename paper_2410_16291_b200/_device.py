@@ -35,13 +35,13 @@ def stream_ptr(device=None) -> int:
     return int(t.cuda.current_stream(device).cuda_stream)
 
 
-# storage dtypes: kernels only see raw pointers, so uint16 travels as int16 and
-# uint64 as int64 (bit-identical views on the host side).
+# storage dtypes: kernels only see raw pointers; uint64 results travel as int64
+# storage (bit-identical views on the host side).
 def storage_dtype(np_dtype: np.dtype):
     t = torch()
     return {
         np.dtype(np.uint8): t.uint8,
-        np.dtype(np.uint16): t.int16,
+        np.dtype(np.uint16): t.uint16,
         np.dtype(np.int32): t.int32,
         np.dtype(np.float32): t.float32,
         np.dtype(np.uint64): t.int64,
@@ -67,14 +67,18 @@ def empty(shape, np_dtype, device, what: str):
 
 def to_device(arr: np.ndarray, device):
     """Host raster -> device tensor (one copy)."""
+    import warnings
+
     t = torch()
-    src = t.from_numpy(np.ascontiguousarray(arr).view(_view_np(arr.dtype)))
+    with warnings.catch_warnings():  # read-only views are only read here
+        warnings.simplefilter("ignore", UserWarning)
+        src = t.from_numpy(np.ascontiguousarray(arr).view(_view_np(arr.dtype)))
     return src.to(device)
 
 
 def _view_np(dt):
     dt = np.dtype(dt)
-    return {np.dtype(np.uint16): np.int16, np.dtype(np.uint64): np.int64}.get(dt, dt)
+    return {np.dtype(np.uint64): np.int64}.get(dt, dt)
 
 
 def to_host(tensor, np_dtype: np.dtype) -> np.ndarray:

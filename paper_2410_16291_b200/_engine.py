@@ -29,8 +29,8 @@ def result_dtype(kind: ElemKind, stat: StatKind) -> np.dtype:
 
 
 def sat_ld_for(cols: int) -> int:
-    """Row pitch of a device table: even (16-byte aligned rows), >= cols + 1."""
-    return (cols + 2) & ~1
+    """Row pitch of a device table: a multiple of 4 elements (32-byte aligned rows), >= cols + 1."""
+    return (cols + 4) & ~3
 
 
 def device_input(img: ImageGrid):

@@ -240,7 +240,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
 
   // band geometry: output rows [o0, o1) need input rows [o0*s, (o1-1)*s + w)
-  const int64_t sat_ld = ((cols + 1) + 1) & ~int64_t(1);
+  const int64_t sat_ld = ((cols + 1) + 3) & ~int64_t(3);  // 32-byte aligned rows
   const int nstats = ((stat_mask & SSB_SUM) ? 1 : 0) + ((stat_mask & SSB_MEAN) ? 1 : 0) + ((stat_mask & SSB_STD) ? 1 : 0);
   auto in_rows_for = [&](int64_t nb) { return (nb - 1) * stride + w; };
   if (band_rows <= 0) {

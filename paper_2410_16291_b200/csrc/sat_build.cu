@@ -4,7 +4,7 @@
 // (pkg/src/satsweep/integral.py:86-116, parallel.py:106-121) with a
 // reduce-then-scan design that writes every table entry exactly once:
 //
-//   phase 1  sat_reduce   per (strip J, segment K) tile: row totals of every
+//   phase 1  sat_reduce   per (strip J, segment K) tile: the total of every
 //                         table row inside the strip and the strip-local
 //                         prefix of the segment's column totals.  Reads the
 //                         image once; writes ~8/TW + 8/SR bytes per pixel.
@@ -13,181 +13,329 @@
 //            sat_segsum   per-(segment, strip) sum of those left carries,
 //            sat_topcarry exclusive scan down the segments of the segment
 //                         column totals (the table row above each segment).
-//   phase 3  sat_scan     per tile: stage RB image rows in shared memory, warp
-//                         row scans, transpose through swizzled smem, column
-//                         accumulation in registers, 128-bit coalesced stores.
+//   phase 3  sat_scan     per tile: warp row scans, transpose through
+//                         swizzled smem, column accumulation in registers,
+//                         128-bit coalesced streaming stores.
+//
+// Both image-reading phases stage RB image rows per step into shared memory
+// with TMA bulk copies (cp.async.bulk, UBLKCP) on a 2-deep mbarrier pipeline,
+// so the global loads of step b+1 are in flight while step b is computed.
+// Rows are copied as the 16-byte-aligned span covering the strip; each lane
+// re-aligns its elements with funnel shifts (the shift is warp-uniform).
 //
 // Table entry for table row i inside segment K and column j inside strip J:
 //   S[i][j] = Top[K][j] + sum_{k0 <= i' <= i} ( RL[J][i'] + RPloc[i'][j] )
 // where RPloc is the strip-local row prefix.  Integer tables are exact modulo
 // 2^64; f32 input accumulates in double with a deterministic order.
+#include <climits>
+
+#include "ssb_async.cuh"
 #include "ssb_common.cuh"
 
 namespace ssb {
 
-// ---- shared memory layout helpers -------------------------------------------
-// Row-scan lanes own E consecutive elements; the transpose buffer uses an XOR
-// swizzle of 16-byte chunks so both the per-lane row writes and the
-// per-thread column reads are bank-conflict free.
-template <int CPL>
-__device__ __forceinline__ int swz_chunk(int c) {
-  if constexpr (CPL <= 1) {
-    return c;
-  } else {
-    const int l = c / CPL, q = c % CPL;
-    const int f = (CPL >= 8) ? (l & 7) : ((l / (8 / CPL)) & (CPL - 1));
-    return l * CPL + (q ^ f);
+// ---- tile geometry -----------------------------------------------------------
+template <typename InT>
+struct Geo {
+  using Tr = Elem<InT>;
+  static constexpr int TW = Tr::kTW;                 // table columns per strip
+  static constexpr int ES = (int)sizeof(InT);        // element bytes
+  static constexpr int E = TW / 32;                  // elements per lane in a row
+  static constexpr int LB = E * ES;                  // bytes per lane (16 or 32)
+  static constexpr int ROWB = TW * ES + 48;          // staged row: 16 B pad + aligned span (<= TW*ES + 32)
+  static constexpr int CPT = TW / kThreads;          // columns per thread in column passes
+};
+
+constexpr int kNoRow = INT_MIN;
+
+// ---- TMA row staging ----------------------------------------------------------
+// Warp 0 stages table rows [r0, r0+nr) x table cols [j0, j0+TW) of the padded
+// image, lane r handling row r (RB <= 32).  offs[r] = byte offset such that
+// image column c of row r sits at stage + r*ROWB + 16 + offs[r] + c*ES
+// (kNoRow: the row has no image data).
+template <typename InT, int RB>
+__device__ __forceinline__ void stage_issue(unsigned char* stage, int* offs, uint64_t* bar, const InT* in, int64_t R,
+                                            int64_t C, int64_t in_ld, int64_t r0, int nr, int64_t j0, int lane) {
+  static_assert(RB <= 32, "one lane per staged row");
+  using G = Geo<InT>;
+  const char* base = reinterpret_cast<const char*>(in);
+  const char* end_valid = base + ((R - 1) * in_ld + C) * G::ES;
+  const int64_t c_lo = j0 > 0 ? j0 - 1 : 0;
+  const int64_t c_hi = (j0 - 1 + G::TW) < C ? (j0 - 1 + G::TW) : C;
+  const int64_t ir = r0 + lane - 1;
+  const bool has = lane < nr && ir >= 0 && ir < R && c_hi > c_lo;
+  const char* a = nullptr;
+  const char* b = nullptr;
+  if (has) {
+    const char* rowp = base + ir * in_ld * G::ES;
+    const char* lo = rowp + c_lo * G::ES;
+    const char* hi = rowp + c_hi * G::ES;
+    a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15));
+    b = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15));
+    if (b > end_valid) {  // never read past the raster: copy the tail bytes by hand
+      b = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(end_valid) & ~uintptr_t(15));
+      if (b < a) b = a;
+      unsigned char* dst = stage + lane * G::ROWB + 16;
+      for (const char* p = b; p < hi; ++p) dst[p - a] = (unsigned char)__ldg(reinterpret_cast<const char*>(p));
+    }
+    offs[lane] = (int)(rowp - a);
+  } else if (lane < RB) {
+    offs[lane] = kNoRow;
+  }
+  uint32_t bytes = has ? (uint32_t)(b - a) : 0u;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, d);
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+  __syncwarp();
+  if (has && b > a) bulk_g2s(stage + lane * G::ROWB + 16, a, (uint32_t)(b - a), bar);
+}
+
+template <int NO, int SW>
+__device__ __forceinline__ void shift_words(const uint32_t* w, uint32_t* o, int sb) {
+#pragma unroll
+  for (int k = 0; k < NO; ++k) o[k] = __funnelshift_r(w[k + SW], w[k + SW + 1], sb);
+}
+
+// Lane's E consecutive elements starting at image column c0 of staged row r,
+// as LB/4 packed 32-bit words.  Columns outside [0, C) and rows without data
+// read as 0.
+template <typename InT> struct Pack {
+  static constexpr int NW = Geo<InT>::LB / 4;  // words per lane
+};
+
+template <typename InT>
+__device__ __forceinline__ InT elem(const uint32_t* o, int k) {
+  if constexpr (sizeof(InT) == 1) return (InT)(o[k >> 2] >> (8 * (k & 3)));
+  else if constexpr (sizeof(InT) == 2) return (InT)(o[k >> 1] >> (16 * (k & 1)));
+  else { InT v; memcpy(&v, &o[k], 4); return v; }
+}
+
+template <typename InT>
+__device__ __forceinline__ void clear_elem(uint32_t* o, int k) {
+  if constexpr (sizeof(InT) == 1) o[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
+  else if constexpr (sizeof(InT) == 2) o[k >> 1] &= ~(0xFFFFu << (16 * (k & 1)));
+  else o[k] = 0u;
+}
+
+template <typename InT>
+__device__ __forceinline__ void lane_words(const unsigned char* stage, const int* offs, int r, int64_t c0, int64_t C,
+                                           uint32_t (&o)[Pack<InT>::NW]) {
+  using G = Geo<InT>;
+  constexpr int NC = G::LB / 16 + 1, NO = Pack<InT>::NW;
+  const int off = offs[r];
+  if (off == kNoRow) {
+#pragma unroll
+    for (int k = 0; k < NO; ++k) o[k] = 0u;
+    return;
+  }
+  const int Q = 16 + off + (int)(c0 * G::ES);
+  const uint4* p = reinterpret_cast<const uint4*>(stage + r * G::ROWB + (Q & ~15));
+  uint32_t w[NC * 4];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const uint4 v = p[c];
+    w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+  }
+  const int s = Q & 15, sb = (s & 3) * 8;
+  switch (s >> 2) {  // warp-uniform: lanes differ by multiples of 16 bytes
+    case 0: shift_words<NO, 0>(w, o, sb); break;
+    case 1: shift_words<NO, 1>(w, o, sb); break;
+    case 2: shift_words<NO, 2>(w, o, sb); break;
+    default: shift_words<NO, 3>(w, o, sb); break;
+  }
+  if (c0 < 0 || c0 + G::E > C) {
+#pragma unroll
+    for (int k = 0; k < G::E; ++k)
+      if (c0 + k < 0 || c0 + k >= C) clear_elem<InT>(o, k);
   }
 }
 
-template <typename T, int TW>
-struct SwzRow {
-  static constexpr int kPerChunk = 16 / sizeof(T);
-  static constexpr int kE = TW / 32;                      // elements per lane
-  static constexpr int kCPL = kE * (int)sizeof(T) / 16;  // 16-byte chunks per lane
-  __device__ static __forceinline__ int idx(int e) {
-    const int c = e / kPerChunk;
-    return swz_chunk<kCPL>(c) * kPerChunk + (e % kPerChunk);
+// sum of the lane's elements in Loc / of their squares in LocSq
+template <typename InT>
+__device__ __forceinline__ typename Elem<InT>::Loc lane_total(const uint32_t* o) {
+  using Loc = typename Elem<InT>::Loc;
+  Loc t = Loc(0);
+  if constexpr (sizeof(InT) == 1) {
+#pragma unroll
+    for (int i = 0; i < Pack<InT>::NW; ++i) t = __dp4a(o[i], 0x01010101u, t);
+  } else {
+#pragma unroll
+    for (int k = 0; k < Geo<InT>::E; ++k) t = add(t, conv<Loc>(elem<InT>(o, k)));
   }
+  return t;
+}
+template <typename InT>
+__device__ __forceinline__ typename Elem<InT>::LocSq lane_total_sq(const uint32_t* o) {
+  using LocSq = typename Elem<InT>::LocSq;
+  LocSq t = LocSq(0);
+  if constexpr (sizeof(InT) == 1) {
+#pragma unroll
+    for (int i = 0; i < Pack<InT>::NW; ++i) t = __dp4a(o[i], o[i], t);
+  } else {
+#pragma unroll
+    for (int k = 0; k < Geo<InT>::E; ++k) t = add(t, convsq<LocSq>(elem<InT>(o, k)));
+  }
+  return t;
+}
+
+template <typename InT>
+__device__ __forceinline__ bool any_nonfinite(const uint32_t* o) {
+  if constexpr (Elem<InT>::kFloat) {
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < Geo<InT>::E; ++k) bad |= !isfinite(elem<InT>(o, k));
+    return bad;
+  } else {
+    return false;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp tiles.  Phases 1 and 3 give every warp its own (strip J, segment K)
+// tile and its own 2-deep TMA row pipeline: the warp sweeps the segment top to
+// bottom, lane l owning E consecutive table columns.  A row's strip-local
+// prefix is a lane-serial prefix plus one warp shuffle scan, and the vertical
+// accumulation happens in the same lane's registers -- no shared-memory
+// transpose and no CTA-wide barrier anywhere in the sweep.
+constexpr int kWarpsPerCta = kThreads / 32;
+
+template <typename InT>
+struct WarpStage {
+  using G = Geo<InT>;
+  static constexpr int RBW = G::ES == 1 ? 8 : 4;  // rows per stage (<= 32)
+  alignas(16) unsigned char buf[2][RBW * G::ROWB];
+  int offs[2][RBW];
+  uint64_t bar[2];
 };
 
-// Stage table rows [r0, r0+nr) x table cols [j0, j0+TW) of the padded image
-// into smem (raw element type).  Element (r, e) <- X'[r0+r][j0+e].
-template <typename InT, int TW, int RB>
-__device__ __forceinline__ void stage_rows(InT (*sin)[TW], const InT* __restrict__ in, int64_t R, int64_t C,
-                                           int64_t in_ld, int64_t r0, int nr, int64_t j0, int tid,
-                                           int* nonfinite_local) {
-  constexpr int kPer = TW / kThreads;
-#pragma unroll 4
-  for (int r = 0; r < nr; ++r) {
-    const int64_t ir = r0 + r - 1;  // image row
-    const bool row_ok = ir >= 0 && ir < R;
-    const InT* rowp = in + ir * in_ld;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = tid + k * kThreads;
-      const int64_t ic = j0 + e - 1;  // image col
-      InT v = InT(0);
-      if (row_ok && ic >= 0 && ic < C) {
-        v = __ldg(rowp + ic);
-        if (is_nonfinite(v)) *nonfinite_local = 1;
-      }
-      sin[r][e] = v;
-    }
+__device__ __forceinline__ void warp_tile(int nJ, int nK, int& J, int& K) {
+  const int t = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  J = t % nJ;
+  K = t / nJ;
+  if (K >= nK) K = -1;
+}
+
+template <typename InT>
+__device__ __forceinline__ void warp_stage_init(WarpStage<InT>& ws, int lane) {
+  if (lane == 0) {
+    mbar_init(&ws.bar[0], 1);
+    mbar_init(&ws.bar[1], 1);
+    fence_mbar_init();
   }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
 // phase 1
 template <typename InT, bool SQ>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads)
 sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                   typename Elem<InT>::Acc* __restrict__ rowtot, typename Elem<InT>::Acc* __restrict__ rowtot_sq,
                   typename Elem<InT>::Acc* __restrict__ colp, typename Elem<InT>::Acc* __restrict__ colp_sq,
-                  int64_t SR, int* __restrict__ nonfinite) {
+                  int64_t SR, int nJ, int nK, int* __restrict__ nonfinite) {
   using Tr = Elem<InT>;
   using Loc = typename Tr::Loc;
   using LocSq = typename Tr::LocSq;
   using Acc = typename Tr::Acc;
-  constexpr int TW = Tr::kTW;
-  constexpr int RB = SQ ? 16 : 32;
-  constexpr int E = TW / 32;
-  constexpr int CPT = TW / kThreads;
-  constexpr int NW = kThreads / 32;
-
-  __shared__ __align__(16) InT sin[RB][TW];
-  __shared__ Acc swarp[2][NW];
-  __shared__ int s_nonfinite;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  using G = Geo<InT>;
+  using WS = WarpStage<InT>;
+  constexpr int TW = G::TW, E = G::E, RB = WS::RBW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WS* stages = reinterpret_cast<WS*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  WS& ws = stages[threadIdx.x >> 5];
+  int J, K;
+  warp_tile(nJ, nK, J, K);
+  if (K < 0) return;
   const int64_t PR = R + 1, PC = C + 1;
-  const int J = blockIdx.x, K = blockIdx.y;
   const int64_t j0 = (int64_t)J * TW, k0 = (int64_t)K * SR;
   const int64_t k1 = min(k0 + SR, PR);
-  if (tid == 0) s_nonfinite = 0;
-  int nf = 0;
+  const int nblk = (int)((k1 - k0 + RB - 1) / RB);
+  const int64_t c0 = j0 + lane * E - 1;
+  bool nf = false;
+  warp_stage_init(ws, lane);
+  stage_issue<InT, RB>(ws.buf[0], ws.offs[0], &ws.bar[0], in, R, C, in_ld, k0, (int)min64(RB, k1 - k0), j0, lane);
 
-  Acc cs[CPT], csq[CPT];
+  Loc cs[E];  // column partials over the segment (<= SR rows: no overflow in Loc / LocSq)
+  LocSq csq[E];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) { cs[c] = Acc(0); csq[c] = Acc(0); }
+  for (int k = 0; k < E; ++k) { cs[k] = Loc(0); csq[k] = LocSq(0); }
 
-  for (int64_t r0 = k0; r0 < k1; r0 += RB) {
-    const int nr = (int)((k1 - r0) < RB ? (k1 - r0) : RB);
-    stage_rows<InT, TW, RB>(sin, in, R, C, in_ld, r0, nr, j0, tid, &nf);
-    __syncthreads();
-    // column totals (thread owns columns tid*CPT ..)
+  for (int b = 0; b < nblk; ++b) {
+    const int s = b & 1;
+    const int64_t r0 = k0 + (int64_t)b * RB;
+    const int nr = (int)min64(RB, k1 - r0);
+    if (b + 1 < nblk) {
+      const int64_t rn = r0 + RB;
+      stage_issue<InT, RB>(ws.buf[s ^ 1], ws.offs[s ^ 1], &ws.bar[s ^ 1], in, R, C, in_ld, rn,
+                           (int)min64(RB, k1 - rn), j0, lane);
+    }
+    mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
+    Acc rtot = Acc(0), rtot_sq = Acc(0);  // lane r keeps the total of row r
     for (int r = 0; r < nr; ++r) {
+      uint32_t o[Pack<InT>::NW];
+      lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const InT x = sin[r][tid * CPT + c];
-        cs[c] = add(cs[c], conv<Acc>(x));
-        if constexpr (SQ) csq[c] = add(csq[c], convsq<Acc>(x));
-      }
-    }
-    // row totals (warp per row, lane owns E consecutive elements)
-    for (int r = warp; r < nr; r += NW) {
-      Loc s = Loc(0);
-      LocSq q = LocSq(0);
+      for (int k = 0; k < E; ++k) cs[k] = add(cs[k], conv<Loc>(elem<InT>(o, k)));
+      const Loc rs = warp_sum(lane_total<InT>(o));
+      if (lane == r) rtot = (Acc)rs;
+      if constexpr (SQ) {
 #pragma unroll
-      for (int k = 0; k < E; ++k) {
-        const InT x = sin[r][lane * E + k];
-        s = add(s, conv<Loc>(x));
-        if constexpr (SQ) q = add(q, convsq<LocSq>(x));
+        for (int k = 0; k < E; ++k) csq[k] = add(csq[k], convsq<LocSq>(elem<InT>(o, k)));
+        const LocSq rq = warp_sum(lane_total_sq<InT>(o));
+        if (lane == r) rtot_sq = (Acc)rq;
       }
-      s = warp_sum(s);
-      if constexpr (SQ) q = warp_sum(q);
-      if (lane == 0) {
-        rowtot[(int64_t)J * PR + r0 + r] = (Acc)s;
-        if constexpr (SQ) rowtot_sq[(int64_t)J * PR + r0 + r] = (Acc)q;
-      }
+      nf |= any_nonfinite<InT>(o);
     }
-    __syncthreads();
+    if (lane < nr) {
+      rowtot[(int64_t)J * PR + r0 + lane] = rtot;
+      if constexpr (SQ) rowtot_sq[(int64_t)J * PR + r0 + lane] = rtot_sq;
+    }
+    __syncwarp();  // stage s fully read before it is refilled
   }
 
-  // block inclusive scan of the column totals across the strip
-  {
-    Acc run = Acc(0), runq = Acc(0);
+  // strip-local prefix of the segment's column totals
+  Acc run = Acc(0), runq = Acc(0);
+  Acc col[E], colq[E];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      run = add(run, cs[c]); cs[c] = run;
-      if constexpr (SQ) { runq = add(runq, csq[c]); csq[c] = runq; }
-    }
-    Acc inc = warp_incl_scan(run, lane);
-    Acc incq = Acc(0);
-    if constexpr (SQ) incq = warp_incl_scan(runq, lane);
-    if (lane == 31) { swarp[0][warp] = inc; if constexpr (SQ) swarp[1][warp] = incq; }
-    __syncthreads();
-    Acc off = sub(inc, run), offq = Acc(0);
-    if constexpr (SQ) offq = sub(incq, runq);
-    for (int w2 = 0; w2 < warp; ++w2) {
-      off = add(off, swarp[0][w2]);
-      if constexpr (SQ) offq = add(offq, swarp[1][w2]);
-    }
+  for (int k = 0; k < E; ++k) {
+    run = add(run, (Acc)cs[k]); col[k] = run;
+    if constexpr (SQ) { runq = add(runq, (Acc)csq[k]); colq[k] = runq; }
+  }
+  const Acc off = sub(warp_incl_scan(run, lane), run);
+  Acc offq = Acc(0);
+  if constexpr (SQ) offq = sub(warp_incl_scan(runq, lane), runq);
+  const int64_t cbase = j0 + lane * E;
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int64_t col = j0 + tid * CPT + c;
-      if (col < PC) {
-        colp[(int64_t)K * PC + col] = add(off, cs[c]);
-        if constexpr (SQ) colp_sq[(int64_t)K * PC + col] = add(offq, csq[c]);
-      }
+  for (int k = 0; k < E; ++k) {
+    if (cbase + k < PC) {
+      colp[(int64_t)K * PC + cbase + k] = add(off, col[k]);
+      if constexpr (SQ) colp_sq[(int64_t)K * PC + cbase + k] = add(offq, colq[k]);
     }
   }
-  if (nf) s_nonfinite = 1;
-  __syncthreads();
-  if (tid == 0 && s_nonfinite && nonfinite) atomicOr(nonfinite, 1);
+  if (nf && nonfinite) atomicOr(nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------
-// phase 2a: left carries (exclusive scan across strips), in place.
+// phase 2a: left carries (exclusive scan across strips), in place.  Loads are
+// batched so each thread keeps several independent requests in flight.
 template <typename Acc>
 __global__ void sat_rowcarry_kernel(Acc* __restrict__ rowtot, int nJ, int64_t PR) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= PR) return;
+  constexpr int B = 8;
   Acc run = Acc(0);
-  for (int J = 0; J < nJ; ++J) {
-    const Acc v = rowtot[(int64_t)J * PR + i];
-    rowtot[(int64_t)J * PR + i] = run;
-    run = add(run, v);
+  for (int J0 = 0; J0 < nJ; J0 += B) {
+    Acc v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) v[k] = (J0 + k < nJ) ? rowtot[(int64_t)(J0 + k) * PR + i] : Acc(0);
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (J0 + k < nJ) rowtot[(int64_t)(J0 + k) * PR + i] = run;
+      run = add(run, v[k]);
+    }
   }
 }
 
@@ -219,124 +367,134 @@ __global__ void sat_topcarry_kernel(Acc* __restrict__ colp, const Acc* __restric
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= PC) return;
   const int J = (int)(j / TW);
+  constexpr int B = 8;
   Acc run = Acc(0);
-  for (int K = 0; K < nK; ++K) {
-    const Acc v = colp[(int64_t)K * PC + j];
-    colp[(int64_t)K * PC + j] = run;
-    run = add(run, add(v, srl[(int64_t)K * nJ + J]));
+  for (int K0 = 0; K0 < nK; K0 += B) {
+    Acc v[B], sr[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      v[k] = (K0 + k < nK) ? colp[(int64_t)(K0 + k) * PC + j] : Acc(0);
+      sr[k] = (K0 + k < nK) ? srl[(int64_t)(K0 + k) * nJ + J] : Acc(0);
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (K0 + k < nK) colp[(int64_t)(K0 + k) * PC + j] = run;
+      run = add(run, add(v[k], sr[k]));
+    }
   }
   if (totals) totals[j] = run;
 }
 
+// adds a carry row to every segment's top row (row-band shards, SURVEY.md 8e)
+template <typename Acc>
+__global__ void sat_apply_carry_kernel(Acc* __restrict__ colp, const Acc* __restrict__ carry, int nK, int64_t PC) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= PC) return;
+  const Acc c = carry[j];
+  for (int K = 0; K < nK; ++K) colp[(int64_t)K * PC + j] = add(colp[(int64_t)K * PC + j], c);
+}
+
 // ---------------------------------------------------------------------------
 // phase 3
-template <typename InT, bool SQ>
-struct ScanSmem {
-  using Tr = Elem<InT>;
-  static constexpr int TW = Tr::kTW;
-  static constexpr int RB = SQ ? 16 : 32;
-  InT sin[RB][TW];
-  typename Tr::Loc rp[RB][TW];
-  typename Tr::LocSq rq[SQ ? RB : 1][SQ ? TW : 1];
-  typename Tr::Acc rl[RB];
-  typename Tr::Acc rlq[RB];
-};
-
-template <typename Acc, int CPT>
-__device__ __forceinline__ void store_cols(Acc* __restrict__ dst, const Acc (&v)[CPT], int64_t col, int64_t PC) {
-  if constexpr (CPT == 2) {
-    if (col + 1 < PC) { st_cs2(dst, v[0], v[1]); return; }
-    if (col < PC) st_cs(dst, v[0]);
+template <typename Acc, int E>
+__device__ __forceinline__ void store_lane_cols(Acc* __restrict__ dst, const Acc (&v)[E], int64_t col, int64_t PC) {
+  if (col + E <= PC) {
+#pragma unroll
+    for (int k = 0; k < E; k += 4) {
+      U64x4 q;
+      memcpy(&q, &v[k], 32);
+      st256(dst + k, q);
+    }
   } else {
-    if (col < PC) st_cs(dst, v[0]);
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (col + k < PC) st_cs(dst + k, v[k]);
   }
 }
 
 template <typename InT, bool SQ>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads)
 sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                 typename Elem<InT>::Acc* __restrict__ sat, typename Elem<InT>::Acc* __restrict__ sat_sq, int64_t sat_ld,
                 const typename Elem<InT>::Acc* __restrict__ rl, const typename Elem<InT>::Acc* __restrict__ rl_sq,
                 const typename Elem<InT>::Acc* __restrict__ top, const typename Elem<InT>::Acc* __restrict__ top_sq,
-                int64_t SR) {
+                int64_t SR, int nJ, int nK) {
   using Tr = Elem<InT>;
   using Loc = typename Tr::Loc;
   using LocSq = typename Tr::LocSq;
   using Acc = typename Tr::Acc;
-  using SM = ScanSmem<InT, SQ>;
-  constexpr int TW = SM::TW, RB = SM::RB, E = TW / 32, CPT = TW / kThreads, NW = kThreads / 32;
-  using SwP = SwzRow<Loc, TW>;
-  using SwQ = SwzRow<LocSq, TW>;
-
+  using G = Geo<InT>;
+  using WS = WarpStage<InT>;
+  constexpr int TW = G::TW, E = G::E, RB = WS::RBW;
+  static_assert(E % 4 == 0, "256-bit stores");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SM& sm = *reinterpret_cast<SM*>(smem_raw);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  WS* stages = reinterpret_cast<WS*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  WS& ws = stages[threadIdx.x >> 5];
+  int J, K;
+  warp_tile(nJ, nK, J, K);
+  if (K < 0) return;
   const int64_t PR = R + 1, PC = C + 1;
-  const int J = blockIdx.x, K = blockIdx.y;
   const int64_t j0 = (int64_t)J * TW, k0 = (int64_t)K * SR;
   const int64_t k1 = min(k0 + SR, PR);
-  const int64_t mycol = j0 + tid * CPT;
-  int nf = 0;
+  const int nblk = (int)((k1 - k0 + RB - 1) / RB);
+  const int64_t cbase = j0 + lane * E;  // table column of the lane's first element
+  const int64_t c0 = cbase - 1;         // matching image column
+  warp_stage_init(ws, lane);
+  stage_issue<InT, RB>(ws.buf[0], ws.offs[0], &ws.bar[0], in, R, C, in_ld, k0, (int)min64(RB, k1 - k0), j0, lane);
 
-  Acc acc[CPT], accq[CPT];
+  Acc acc[E], accq[E];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int64_t col = mycol + c;
-    acc[c] = col < PC ? top[(int64_t)K * PC + col] : Acc(0);
-    if constexpr (SQ) accq[c] = col < PC ? top_sq[(int64_t)K * PC + col] : Acc(0);
+  for (int k = 0; k < E; ++k) {
+    acc[k] = cbase + k < PC ? top[(int64_t)K * PC + cbase + k] : Acc(0);
+    if constexpr (SQ) accq[k] = cbase + k < PC ? top_sq[(int64_t)K * PC + cbase + k] : Acc(0);
   }
+  const bool writes_plain = sat != nullptr;
 
-  for (int64_t r0 = k0; r0 < k1; r0 += RB) {
-    const int nr = (int)((k1 - r0) < RB ? (k1 - r0) : RB);
-    stage_rows<InT, TW, RB>(sm.sin, in, R, C, in_ld, r0, nr, j0, tid, &nf);
-    if (tid < nr) {
-      sm.rl[tid] = rl[(int64_t)J * PR + r0 + tid];
-      if constexpr (SQ) sm.rlq[tid] = rl_sq[(int64_t)J * PR + r0 + tid];
+  for (int b = 0; b < nblk; ++b) {
+    const int s = b & 1;
+    const int64_t r0 = k0 + (int64_t)b * RB;
+    const int nr = (int)min64(RB, k1 - r0);
+    if (b + 1 < nblk) {
+      const int64_t rn = r0 + RB;
+      stage_issue<InT, RB>(ws.buf[s ^ 1], ws.offs[s ^ 1], &ws.bar[s ^ 1], in, R, C, in_ld, rn,
+                           (int)min64(RB, k1 - rn), j0, lane);
     }
-    __syncthreads();
-
-    // strip-local row prefixes, one warp per row
-    for (int r = warp; r < nr; r += NW) {
-      Loc p[E];
-      LocSq q[E];
-      Loc s = Loc(0);
-      LocSq sq = LocSq(0);
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        const InT x = sm.sin[r][lane * E + k];
-        s = add(s, conv<Loc>(x)); p[k] = s;
-        if constexpr (SQ) { sq = add(sq, convsq<LocSq>(x)); q[k] = sq; }
-      }
-      const Loc off = sub(warp_incl_scan(s, lane), s);
-      LocSq offq = LocSq(0);
-      if constexpr (SQ) offq = sub(warp_incl_scan(sq, lane), sq);
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        sm.rp[r][SwP::idx(lane * E + k)] = add(off, p[k]);
-        if constexpr (SQ) sm.rq[r][SwQ::idx(lane * E + k)] = add(offq, q[k]);
-      }
+    Acc rlv = Acc(0), rlqv = Acc(0);  // lane r: left carry of row r
+    if (lane < nr) {
+      rlv = rl[(int64_t)J * PR + r0 + lane];
+      if constexpr (SQ) rlqv = rl_sq[(int64_t)J * PR + r0 + lane];
     }
-    __syncthreads();
-
-    // column accumulation + stores
+    mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
     for (int r = 0; r < nr; ++r) {
-      const Acc rlv = sm.rl[r];
-      Acc rlqv = Acc(0);
-      if constexpr (SQ) rlqv = sm.rlq[r];
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const int e = tid * CPT + c;
-        acc[c] = add(acc[c], add(rlv, (Acc)sm.rp[r][SwP::idx(e)]));
-        if constexpr (SQ) accq[c] = add(accq[c], add(rlqv, (Acc)sm.rq[r][SwQ::idx(e)]));
-      }
+      uint32_t o[Pack<InT>::NW];
+      lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
       const int64_t row = r0 + r;
-      if (sat != nullptr) store_cols<Acc, CPT>(sat + row * sat_ld + mycol, acc, mycol, PC);
-      if constexpr (SQ) store_cols<Acc, CPT>(sat_sq + row * sat_ld + mycol, accq, mycol, PC);
+      {
+        const Loc t = lane_total<InT>(o);
+        Loc run = sub(warp_incl_scan(t, lane), t);  // exclusive: prefix of the lanes to the left
+        const Acc left = __shfl_sync(0xffffffffu, rlv, r);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          run = add(run, conv<Loc>(elem<InT>(o, k)));
+          acc[k] = add(acc[k], add(left, (Acc)run));
+        }
+        if (writes_plain) store_lane_cols<Acc, E>(sat + row * sat_ld + cbase, acc, cbase, PC);
+      }
+      if constexpr (SQ) {
+        const LocSq t = lane_total_sq<InT>(o);
+        LocSq run = sub(warp_incl_scan(t, lane), t);
+        const Acc left = __shfl_sync(0xffffffffu, rlqv, r);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          run = add(run, convsq<LocSq>(elem<InT>(o, k)));
+          accq[k] = add(accq[k], add(left, (Acc)run));
+        }
+        store_lane_cols<Acc, E>(sat_sq + row * sat_ld + cbase, accq, cbase, PC);
+      }
     }
-    __syncthreads();
+    __syncwarp();  // stage s fully read before it is refilled
   }
-  (void)nf;
 }
 
 // ---------------------------------------------------------------------------
@@ -355,8 +513,8 @@ inline SatPlan make_sat_plan(int dtype, int64_t R, int64_t C, bool sq) {
   p.TW = tw_for(dtype);
   p.PR = R + 1; p.PC = C + 1;
   p.nJ = (int)((p.PC + p.TW - 1) / p.TW);
-  const int RB = sq ? 16 : 32;
-  const int64_t target_tiles = 4 * kNumSMs;
+  const int RB = 8;  // segment height is a multiple of every kernel's row block
+  const int64_t target_tiles = 64LL * kNumSMs;  // warp tiles: ~4 waves of 16 warps per SM
   int64_t wantK = (target_tiles + p.nJ - 1) / p.nJ;
   int64_t SR = (p.PR + wantK - 1) / wantK;
   SR = ((SR + RB - 1) / RB) * RB;
@@ -375,14 +533,6 @@ inline SatPlan make_sat_plan(int dtype, int64_t R, int64_t C, bool sq) {
   return p;
 }
 
-// adds a carry row to every segment's top row (row-band shards, SURVEY.md 8e)
-template <typename Acc>
-__global__ void sat_apply_carry_kernel(Acc* __restrict__ colp, const Acc* __restrict__ carry, int nK, int64_t PC) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= PC) return;
-  const Acc c = carry[j];
-  for (int K = 0; K < nK; ++K) colp[(int64_t)K * PC + j] = add(colp[(int64_t)K * PC + j], c);
-}
 
 template <typename InT, bool SQ>
 cudaError_t launch_sat_prepare_t(const void* in, int64_t R, int64_t C, int64_t in_ld, void* ws, void* totals,
@@ -397,7 +547,12 @@ cudaError_t launch_sat_prepare_t(const void* in, int64_t R, int64_t C, int64_t i
   Acc* srl_sq = SQ ? w + p.off_srl_sq : nullptr;
   const InT* x = reinterpret_cast<const InT*>(in);
   dim3 grid(p.nJ, p.nK);
-  sat_reduce_kernel<InT, SQ><<<grid, kThreads, 0, st>>>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, nonfinite);
+  const int tb = (int)(((int64_t)p.nJ * p.nK + kWarpsPerCta - 1) / kWarpsPerCta);
+  const int smem = (int)(sizeof(WarpStage<InT>) * kWarpsPerCta);
+  cudaError_t e = cudaFuncSetAttribute(sat_reduce_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  sat_reduce_kernel<InT, SQ><<<tb, kThreads, smem, st>>>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ,
+                                                      p.nK, nonfinite);
   const int nb_rows = (int)((p.PR + kThreads - 1) / kThreads);
   sat_rowcarry_kernel<Acc><<<nb_rows, kThreads, 0, st>>>(rowtot, p.nJ, p.PR);
   if (SQ) sat_rowcarry_kernel<Acc><<<nb_rows, kThreads, 0, st>>>(rowtot_sq, p.nJ, p.PR);
@@ -423,24 +578,24 @@ cudaError_t launch_sat_finish_t(const void* in, int64_t R, int64_t C, int64_t in
   const int nb_cols = (int)((p.PC + kThreads - 1) / kThreads);
   if (carry) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp, reinterpret_cast<const Acc*>(carry), p.nK, p.PC); note_launch(1); }
   if (SQ && carry_sq) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp_sq, reinterpret_cast<const Acc*>(carry_sq), p.nK, p.PC); note_launch(1); }
-  const size_t smem = sizeof(ScanSmem<InT, SQ>);
-  auto kfn = sat_scan_kernel<InT, SQ>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int tb = (int)(((int64_t)p.nJ * p.nK + kWarpsPerCta - 1) / kWarpsPerCta);
+  const int smem = (int)(sizeof(WarpStage<InT>) * kWarpsPerCta);
+  cudaError_t e = cudaFuncSetAttribute(sat_scan_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(p.nJ, p.nK);
-  kfn<<<grid, kThreads, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld, reinterpret_cast<Acc*>(sat),
-                                    reinterpret_cast<Acc*>(sat_sq), sat_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR);
+  sat_scan_kernel<InT, SQ><<<tb, kThreads, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
+                                                    reinterpret_cast<Acc*>(sat), reinterpret_cast<Acc*>(sat_sq),
+                                                    sat_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ, p.nK);
   note_launch(1);
   return cudaGetLastError();
 }
 
-#define SSB_SAT_DISPATCH(CALL_T)                                  \
-  switch (dtype) {                                                \
+#define SSB_SAT_DISPATCH(CALL_T)                                                \
+  switch (dtype) {                                                              \
     case IN_U8: return sq ? CALL_T(uint8_t, true) : CALL_T(uint8_t, false);     \
     case IN_U16: return sq ? CALL_T(uint16_t, true) : CALL_T(uint16_t, false);  \
     case IN_I32: return sq ? CALL_T(int32_t, true) : CALL_T(int32_t, false);    \
     case IN_F32: return sq ? CALL_T(float, true) : CALL_T(float, false);        \
-    default: return cudaErrorInvalidValue;                        \
+    default: return cudaErrorInvalidValue;                                      \
   }
 
 cudaError_t launch_sat_prepare(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, bool sq, void* ws,

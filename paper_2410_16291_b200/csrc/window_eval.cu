@@ -12,6 +12,10 @@
 // strides over them.  A table row is first read as the bottom corner row of
 // output row i-w and re-read from L2 as the top corner row of output row i, so
 // HBM sees each table byte about once.
+#include <atomic>
+#include <cstdlib>
+
+#include "ssb_async.cuh"
 #include "ssb_common.cuh"
 
 namespace ssb {
@@ -22,6 +26,8 @@ struct EvalGeom {
   int64_t n_panels, cpp, cpl;  // chunks per full panel / in the last panel
   int64_t n_items;
   int mask;
+  int vec_out;  // output rows aligned for VW-wide stores
+  int hints;    // L2 policy: 0 none, 1 bottom evict_last + top evict_first, 2 top evict_first only
 };
 
 constexpr int kChunk = 2 * kThreads;  // 512 output columns per work item
@@ -77,48 +83,6 @@ template <typename Acc> struct Pair;
 template <> struct Pair<uint64_t> { using V = ulonglong2; };
 template <> struct Pair<double> { using V = double2; };
 
-// Vector path: stride 1, even window, even sat_ld -> all four corner pairs are
-// 16-byte aligned.
-template <typename Acc, bool SQ>
-__global__ void __launch_bounds__(kThreads)
-window_eval_vec_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, EvalGeom g, WinOut o, Fin<Acc> fin) {
-  using V = typename Pair<Acc>::V;
-  const bool vec_out = ((o.ld & 1) == 0);
-  for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
-    int64_t i, cb;
-    decode_item(g, it, i, cb);
-    const int64_t j = cb + 2 * threadIdx.x;
-    if (j >= g.out_c) continue;
-    const bool two = (j + 1) < g.out_c;
-    const int64_t top = i * g.sat_ld, bot = (i + g.w) * g.sat_ld;
-    Acc s0, s1, q0 = Acc(0), q1 = Acc(0);
-    if (two) {
-      const V tl = __ldg(reinterpret_cast<const V*>(sat + top + j));
-      const V tr = __ldg(reinterpret_cast<const V*>(sat + top + j + g.w));
-      const V bl = __ldg(reinterpret_cast<const V*>(sat + bot + j));
-      const V br = __ldg(reinterpret_cast<const V*>(sat + bot + j + g.w));
-      s0 = corner4<Acc>(br.x, tr.x, bl.x, tl.x);
-      s1 = corner4<Acc>(br.y, tr.y, bl.y, tl.y);
-      if constexpr (SQ) {
-        const V qtl = __ldg(reinterpret_cast<const V*>(sq + top + j));
-        const V qtr = __ldg(reinterpret_cast<const V*>(sq + top + j + g.w));
-        const V qbl = __ldg(reinterpret_cast<const V*>(sq + bot + j));
-        const V qbr = __ldg(reinterpret_cast<const V*>(sq + bot + j + g.w));
-        q0 = corner4<Acc>(qbr.x, qtr.x, qbl.x, qtl.x);
-        q1 = corner4<Acc>(qbr.y, qtr.y, qbl.y, qtl.y);
-      }
-    } else {
-      s0 = corner4(__ldg(sat + bot + j + g.w), __ldg(sat + top + j + g.w), __ldg(sat + bot + j), __ldg(sat + top + j));
-      s1 = s0;
-      if constexpr (SQ) {
-        q0 = corner4(__ldg(sq + bot + j + g.w), __ldg(sq + top + j + g.w), __ldg(sq + bot + j), __ldg(sq + top + j));
-        q1 = q0;
-      }
-    }
-    emit_pair<Acc>(g, o, fin, i, j, s0, s1, q0, q1, two, vec_out);
-  }
-}
-
 // General path: any stride / odd window; two outputs per thread, strided.
 template <typename Acc, bool SQ>
 __global__ void __launch_bounds__(kThreads)
@@ -138,6 +102,289 @@ window_eval_gen_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
       emit_pair<Acc>(g, o, fin, i, j, s0, s0, q0, q0, false, false);
     }
   }
+}
+
+// Row-sweep path (stride 1).  CTA b owns chunk (b % cpp) of every panel and
+// visits output rows q, q+k, q+2k, ... (q = b / cpp, k = gridDim / cpp); all
+// CTAs are resident at once, so the rows in flight form a narrow band of one
+// panel and the top corner row of output row i (loaded as a bottom row w rows
+// earlier) is served from L2.  Lane l of warp v evaluates outputs
+// j = chunk + 128 v + l + 32 u (u < 4): every corner load and every store is a
+// fully coalesced 256-byte warp access, whatever the alignment of the output
+// rows (a contiguous 69,745 x 84,745 result has 8-byte-aligned rows), and each
+// thread keeps 16 independent loads in flight.  No integer division in the loop.
+constexpr int kOutPerThread = 4;
+constexpr int kRowChunk = kThreads * kOutPerThread;  // 1024 outputs per CTA row step
+
+__device__ __forceinline__ uint64_t ldg_hint(const uint64_t* p, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_hint(const double* p, uint64_t pol) {
+  return __longlong_as_double((long long)ldg_hint(reinterpret_cast<const uint64_t*>(p), pol));
+}
+
+template <typename Acc, bool SQ>
+__global__ void __launch_bounds__(kThreads)
+window_eval_rows_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, EvalGeom g, WinOut o, Fin<Acc> fin) {
+  constexpr int U = kOutPerThread;
+  const int cpp = (int)g.cpp;
+  const int c = blockIdx.x % cpp;
+  const int q = blockIdx.x / cpp;
+  const int k = gridDim.x / cpp;
+  if (q >= k) return;
+  const uint64_t keep = g.hints == 1 ? policy_evict_last() : policy_evict_normal();
+  const uint64_t drop = g.hints == 0 ? policy_evict_normal() : policy_evict_first();
+  const int64_t w = g.w, ld = g.sat_ld;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t p = 0; p < g.n_panels; ++p) {
+    const int64_t chunks = (p == g.n_panels - 1) ? g.cpl : g.cpp;
+    if (c >= chunks) continue;
+    const int64_t jb = p * g.pw + (int64_t)c * kRowChunk + warp * (32 * U) + lane;
+    if (jb >= g.out_c) continue;
+    const bool full = jb + 32 * (U - 1) < g.out_c;
+#pragma unroll 2
+    for (int64_t i = q; i < g.out_r; i += k) {
+      const Acc* top = sat + i * ld + jb;
+      const Acc* bot = top + w * ld;
+      Acc s[U], qq[U];
+      if (full) {
+        Acc tl[U], tr[U], bl[U], br[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          tl[u] = ldg_hint(top + 32 * u, drop);
+          tr[u] = ldg_hint(top + 32 * u + w, drop);
+          bl[u] = ldg_hint(bot + 32 * u, keep);
+          br[u] = ldg_hint(bot + 32 * u + w, keep);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s[u] = corner4<Acc>(br[u], tr[u], bl[u], tl[u]);
+        if constexpr (SQ) {
+          const Acc* qt = sq + i * ld + jb;
+          const Acc* qb = qt + w * ld;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            tl[u] = ldg_hint(qt + 32 * u, drop);
+            tr[u] = ldg_hint(qt + 32 * u + w, drop);
+            bl[u] = ldg_hint(qb + 32 * u, keep);
+            br[u] = ldg_hint(qb + 32 * u + w, keep);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) qq[u] = corner4<Acc>(br[u], tr[u], bl[u], tl[u]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (jb + 32 * u < g.out_c) {
+            const int64_t d = 32 * u;
+            s[u] = corner4<Acc>(__ldg(bot + d + w), __ldg(top + d + w), __ldg(bot + d), __ldg(top + d));
+            if constexpr (SQ) {
+              const Acc* qt = sq + i * ld + jb;
+              const Acc* qb = qt + w * ld;
+              qq[u] = corner4<Acc>(__ldg(qb + d + w), __ldg(qt + d + w), __ldg(qb + d), __ldg(qt + d));
+            }
+          }
+        }
+      }
+      const int64_t base = i * o.ld + jb;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!full && jb + 32 * u >= g.out_c) break;
+        const int64_t at = base + 32 * u;
+        if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, s[u]);
+        if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(s[u]));
+        if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(s[u], qq[u]));
+      }
+    }
+  }
+}
+
+// panel width (output columns, multiple of `chunk`) that keeps the w+1 table
+// rows a panel touches (both tables) within ~`budget` bytes of L2
+inline int64_t panel_width(int64_t out_c, int64_t w, int64_t s, bool sq, int64_t chunk, double budget) {
+  const double row_bytes = 8.0 * (sq ? 2 : 1) * (double)(w * s + 1);
+  int64_t pw = (int64_t)(budget / row_bytes);
+  pw = (pw / chunk) * chunk;
+  if (pw < chunk) pw = chunk;
+  const int64_t full = ((out_c + chunk - 1) / chunk) * chunk;
+  return pw > full ? full : pw;
+}
+
+// TMA path (stride 1, moderate w): per row step the CTA bulk-copies the top and
+// bottom table row segments [j0, j0 + CW + w) into shared memory (cp.async.bulk,
+// 4-stage full/empty mbarrier ring driven by one producer thread), then every
+// thread evaluates outputs j0 + t + 256 u from shared memory and streams them
+// out with coalesced stores.  Each table byte crosses L2->SM about
+// (CW + w) / CW times per row instead of twice, and the copy engine keeps tens
+// of KB per SM in flight without occupying load slots.
+constexpr int kTmaMaxNS = 8;  // pipeline depth (runtime, <= 8)
+
+struct TmaPlan {
+  int64_t seg;     // elements per staged row segment (even)
+  int64_t steps;   // row steps per CTA (upper bound, all panels)
+  int ntab;        // 1 (sum) or 2 (sum + squares)
+};
+
+// Work items (panel, output row, chunk) are handed out in that order by an
+// atomic ticket, so the items in flight are always a contiguous range of the
+// global order: the rows being evaluated stay a narrow band of one panel and a
+// table row fetched as a bottom corner row is still in L2 when it is needed as
+// a top corner row w rows later (a static assignment lets CTAs drift apart).
+__device__ unsigned long long g_eval_tickets[256];
+
+template <typename Acc, bool SQ, int U>
+__global__ void __launch_bounds__(kThreads)
+window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, EvalGeom g, WinOut o, Fin<Acc> fin,
+                       int64_t seg, unsigned long long* __restrict__ ticket, int NS, int batch) {
+  constexpr int NT = SQ ? 2 : 1;
+  constexpr int kTmaCW = kThreads * U;  // outputs per row step
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + kTmaMaxNS;
+  int64_t* meta = reinterpret_cast<int64_t*>(empty + kTmaMaxNS);  // [NS] item of each stage (-1: done)
+  Acc* buf = reinterpret_cast<Acc*>(smem_raw + 256);              // [NS][NT][2][seg]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t w = g.w, ld = g.sat_ld;
+  const int64_t per_panel = g.out_r * g.cpp;
+  const int64_t total = per_panel * (g.n_panels - 1) + g.out_r * g.cpl;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto coords = [&](int64_t it, int64_t& i, int64_t& j0) {
+    const int64_t p = it / per_panel;
+    const int64_t rem = it - p * per_panel;
+    const int64_t cpp = (p == g.n_panels - 1) ? g.cpl : g.cpp;
+    i = rem / cpp;
+    j0 = p * g.pw + (rem - i * cpp) * kTmaCW;
+  };
+  bool producing = true;
+  // tickets come in batches of `batch` consecutive items (one atomic per
+  // batch); the next batch is requested while the current one is issued
+  int64_t cur = 0, cur_end = 0, next_b = 0;
+  if (tid == 0) {
+    next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+  }
+  auto produce = [&](int64_t m) {  // thread 0 only
+    const int s = (int)(m % NS);
+    if (m >= NS) mbar_wait(&empty[s], (uint32_t)(((m / NS) - 1) & 1));
+    if (cur == cur_end) {
+      cur = next_b;
+      cur_end = next_b + batch;
+      if (cur < total) next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+    }
+    const int64_t it = cur++;
+    if (it >= total) {
+      meta[s] = -1;
+      producing = false;
+      mbar_arrive_expect_tx(&full[s], 0);
+      return;
+    }
+    meta[s] = it;
+    int64_t i, j0;
+    coords(it, i, j0);
+    int64_t len = ld - j0 < seg ? ld - j0 : seg;
+    len &= ~int64_t(1);
+    const uint32_t bytes = (uint32_t)(len * 8);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[s], bytes * 2 * NT);
+    Acc* b = buf + (int64_t)s * NT * 2 * seg;
+    bulk_g2s(b, sat + i * ld + j0, bytes, &full[s]);
+    bulk_g2s(b + seg, sat + (i + w) * ld + j0, bytes, &full[s]);
+    if constexpr (SQ) {
+      bulk_g2s(b + 2 * seg, sq + i * ld + j0, bytes, &full[s]);
+      bulk_g2s(b + 3 * seg, sq + (i + w) * ld + j0, bytes, &full[s]);
+    }
+  };
+  if (tid == 0)
+    for (int64_t m = 0; m < NS - 1 && producing; ++m) produce(m);
+  for (int64_t m = 0;; ++m) {
+    if (tid == 0 && producing) produce(m + NS - 1);
+    const int s = (int)(m % NS);
+    mbar_wait(&full[s], (uint32_t)((m / NS) & 1));
+    const int64_t it = meta[s];
+    if (it < 0) break;
+    int64_t i, j0;
+    coords(it, i, j0);
+    const Acc* T = buf + (int64_t)s * NT * 2 * seg;
+    const Acc* B = T + seg;
+    Acc sv[U], qv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int jj = tid + kThreads * u;
+      sv[u] = corner4<Acc>(B[jj + w], T[jj + w], B[jj], T[jj]);
+      if constexpr (SQ) {
+        const Acc* TQ = T + 2 * seg;
+        const Acc* BQ = T + 3 * seg;
+        qv[u] = corner4<Acc>(BQ[jj + w], TQ[jj + w], BQ[jj], TQ[jj]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    const int64_t base = i * o.ld + j0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + tid + kThreads * u;
+      if (j >= g.out_c) break;
+      const int64_t at = base + tid + kThreads * u;
+      if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, sv[u]);
+      if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(sv[u]));
+      if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(sv[u], qv[u]));
+    }
+  }
+}
+
+template <typename Acc, bool SQ, int U>
+cudaError_t launch_tma_u(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, cudaStream_t st,
+                       bool& used) {
+  used = false;
+  constexpr int NT = SQ ? 2 : 1;
+  constexpr int64_t kTmaCW = kThreads * U;
+  const int64_t seg = (kTmaCW + g.w + 1) & ~int64_t(1);
+  const char* env_b = getenv("SSB_EVAL_BATCH");
+  const int batch = env_b ? atoi(env_b) : 4;
+  const char* env_ns = getenv("SSB_EVAL_STAGES");
+  int NS = env_ns ? atoi(env_ns) : 2;
+  if (NS < 2) NS = 2;
+  if (NS > kTmaMaxNS) NS = kTmaMaxNS;
+  const size_t smem = 256 + (size_t)NS * NT * 2 * seg * sizeof(Acc);
+  if (smem > 200 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) || (SQ && (reinterpret_cast<uintptr_t>(sat_sq) & 15)) ||
+      (g.sat_ld & 1))
+    return cudaSuccess;
+  const char* env_mb = getenv("SSB_EVAL_L2_MB");
+  const char* env_k = getenv("SSB_EVAL_ROWS_IN_FLIGHT");
+  const char* env_h = getenv("SSB_EVAL_HINTS");
+  g.hints = env_h ? atoi(env_h) : 0;
+  g.pw = panel_width(g.out_c, g.w, 1, SQ, kTmaCW, (env_mb ? atof(env_mb) : 8.0) * 1024 * 1024);
+  g.n_panels = (g.out_c + g.pw - 1) / g.pw;
+  g.cpp = g.pw / kTmaCW;
+  g.cpl = (g.out_c - (g.n_panels - 1) * g.pw + kTmaCW - 1) / kTmaCW;
+  auto kfn = window_eval_tma_kernel<Acc, SQ, U>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads, smem);
+  if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+  int blocks = kNumSMs * per_sm;
+  if (env_k && atoi(env_k) > 0 && atoi(env_k) < blocks) blocks = atoi(env_k);
+  // one ticket counter per launch, from a small ring (concurrent launches on
+  // different streams get different slots)
+  static std::atomic<unsigned> slot{0};
+  unsigned long long* tickets = nullptr;
+  e = cudaGetSymbolAddress(reinterpret_cast<void**>(&tickets), g_eval_tickets);
+  if (e != cudaSuccess) return e;
+  unsigned long long* ticket = tickets + (slot.fetch_add(1) % 256);
+  e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  kfn<<<blocks, kThreads, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq), g, o,
+                                      fin, seg, ticket, NS, batch);
+  used = true;
+  return cudaGetLastError();
 }
 
 inline EvalGeom make_eval_geom(int64_t R, int64_t C, int64_t w, int64_t s, int64_t sat_ld, int mask, bool sq) {
@@ -162,50 +409,85 @@ inline EvalGeom make_eval_geom(int64_t R, int64_t C, int64_t w, int64_t s, int64
   return g;
 }
 
+template <typename Acc, bool SQ>
+cudaError_t launch_tma(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, cudaStream_t st,
+                       bool& used) {
+  const char* env_u = getenv("SSB_EVAL_UNROLL");
+  const int u = env_u ? atoi(env_u) : 4;
+  if (u == 8) return launch_tma_u<Acc, SQ, 8>(sat, sat_sq, g, o, fin, st, used);
+  if (u == 2) return launch_tma_u<Acc, SQ, 2>(sat, sat_sq, g, o, fin, st, used);
+  return launch_tma_u<Acc, SQ, 4>(sat, sat_sq, g, o, fin, st, used);
+}
+
+template <typename Acc, bool SQ>
+cudaError_t launch_rows(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, cudaStream_t st) {
+  constexpr int64_t CH = kRowChunk;
+  const char* env_mb = getenv("SSB_EVAL_L2_MB");
+  const char* env_k = getenv("SSB_EVAL_ROWS_IN_FLIGHT");
+  const char* env_h = getenv("SSB_EVAL_HINTS");
+  g.hints = env_h ? atoi(env_h) : 2;
+  g.pw = panel_width(g.out_c, g.w, 1, SQ, CH, (env_mb ? atof(env_mb) : 24.0) * 1024 * 1024);
+  g.n_panels = (g.out_c + g.pw - 1) / g.pw;
+  g.cpp = g.pw / CH;
+  g.cpl = (g.out_c - (g.n_panels - 1) * g.pw + CH - 1) / CH;
+  // persistent grid: every CTA resident at once, so the rows in flight stay a
+  // narrow band and the panel's w table rows stay in L2
+  int per_sm = 0;
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, window_eval_rows_kernel<Acc, SQ>,
+                                                                 kThreads, 0);
+  if (oe != cudaSuccess || per_sm < 1) per_sm = 1;
+  int64_t k = (int64_t)kNumSMs * per_sm / g.cpp;
+  if (env_k && atoi(env_k) > 0 && atoi(env_k) < k) k = atoi(env_k);
+  if (k < 1) k = 1;
+  if (k > g.out_r) k = g.out_r;
+  const int blocks = (int)(k * g.cpp);
+  window_eval_rows_kernel<Acc, SQ><<<blocks, kThreads, 0, st>>>(reinterpret_cast<const Acc*>(sat),
+                                                               reinterpret_cast<const Acc*>(sat_sq), g, o, fin);
+  return cudaGetLastError();
+}
+
+template <typename Acc>
+cudaError_t launch_eval_t(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, bool sq, cudaStream_t st) {
+  if (g.s == 1) {
+    const char* env_path = getenv("SSB_EVAL_PATH");  // tuning: "ldg" forces the load-based sweep
+    if (!(env_path && env_path[0] == 'l')) {
+      bool used = false;
+      cudaError_t e = sq ? launch_tma<Acc, true>(sat, sat_sq, g, o, fin, st, used)
+                         : launch_tma<Acc, false>(sat, sat_sq, g, o, fin, st, used);
+      if (e != cudaSuccess || used) return e;
+    }
+    return sq ? launch_rows<Acc, true>(sat, sat_sq, g, o, fin, st) : launch_rows<Acc, false>(sat, sat_sq, g, o, fin, st);
+  }
+  const int64_t max_blocks = (int64_t)kNumSMs * 8;
+  const int blocks = (int)(g.n_items < max_blocks ? g.n_items : max_blocks);
+  const Acc* x = reinterpret_cast<const Acc*>(sat);
+  const Acc* y = reinterpret_cast<const Acc*>(sat_sq);
+  if (sq) window_eval_gen_kernel<Acc, true><<<blocks, kThreads, 0, st>>>(x, y, g, o, fin);
+  else window_eval_gen_kernel<Acc, false><<<blocks, kThreads, 0, st>>>(x, y, g, o, fin);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R, int64_t C,
                                int64_t sat_ld, int64_t w, int64_t s, int mask, WinOut o, cudaStream_t st) {
   const bool sq = (mask & ST_STD) != 0;
   const EvalGeom g = make_eval_geom(R, C, w, s, sat_ld, mask, sq);
   if (g.n_items <= 0) return cudaSuccess;
-  const bool vec = (s == 1) && ((w & 1) == 0) && ((sat_ld & 1) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(sat) & 15) == 0) &&
-                   (!sq || (reinterpret_cast<uintptr_t>(sat_sq) & 15) == 0);
-  const int64_t max_blocks = (int64_t)kNumSMs * 8;
-  const int blocks = (int)(g.n_items < max_blocks ? g.n_items : max_blocks);
-  const double dn = (double)(w * w);
+  cudaError_t e;
   if (is_float) {
-    Fin<double> fin{dn};
-    const double* a = reinterpret_cast<const double*>(sat);
-    const double* b = reinterpret_cast<const double*>(sat_sq);
-    if (vec) { if (sq) window_eval_vec_kernel<double, true><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin);
-               else window_eval_vec_kernel<double, false><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin); }
-    else { if (sq) window_eval_gen_kernel<double, true><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin);
-           else window_eval_gen_kernel<double, false><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin); }
+    Fin<double> fin{(double)(w * w)};
+    e = launch_eval_t<double>(sat, sat_sq, g, o, fin, sq, st);
   } else {
     Fin<uint64_t> fin{};
     fin.f.n = (uint64_t)(w * w);
-    fin.f.dn = dn;
-    const double maxv = in_dtype == IN_U8 ? 255.0 : in_dtype == IN_U16 ? 65535.0 : 2147483648.0;
-    // w^4 * max^2 <= 2^64 - 1, evaluated exactly in 128-bit integers
-    {
-      unsigned __int128 ww = (unsigned __int128)(uint64_t)w * (uint64_t)w;
-      unsigned __int128 m = (unsigned __int128)(uint64_t)maxv;
-      bool ok = true;
-      // (ww*m)^2 <= lim  <=>  ww*m <= floor(sqrt(lim)) = 2^32 - 1 (exact since lim = 2^64-1)
-      unsigned __int128 a = ww * m;
-      if (a > (unsigned __int128)0xFFFFFFFFull) ok = false;
-      fin.f.u64_ok = ok;
-    }
+    fin.f.dn = (double)(w * w);
+    const uint64_t maxv = in_dtype == IN_U8 ? 255u : in_dtype == IN_U16 ? 65535u : 2147483648u;
+    // stats.py:28-32: w^4 * max^2 <= 2^64 - 1  <=>  w^2 * max <= 2^32 - 1
+    fin.f.u64_ok = ((unsigned __int128)(uint64_t)(w * w) * maxv) <= (unsigned __int128)0xFFFFFFFFull;
     fin.f.is_signed = (in_dtype == IN_I32);
-    const uint64_t* a = reinterpret_cast<const uint64_t*>(sat);
-    const uint64_t* b = reinterpret_cast<const uint64_t*>(sat_sq);
-    if (vec) { if (sq) window_eval_vec_kernel<uint64_t, true><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin);
-               else window_eval_vec_kernel<uint64_t, false><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin); }
-    else { if (sq) window_eval_gen_kernel<uint64_t, true><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin);
-           else window_eval_gen_kernel<uint64_t, false><<<blocks, kThreads, 0, st>>>(a, b, g, o, fin); }
+    e = launch_eval_t<uint64_t>(sat, sat_sq, g, o, fin, sq, st);
   }
   note_launch(1);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace ssb
