@@ -227,6 +227,50 @@ __device__ __forceinline__ void warp_stage_init(WarpStage<InT>& ws, int lane) {
   __syncwarp();
 }
 
+template <int N, int OFF, typename T>
+__device__ __forceinline__ T warp_reduce_scatter_step(T (&v)[N], int lane) {
+  if constexpr (N == 1) {
+    T x = v[0];
+#pragma unroll
+    for (int d = OFF; d >= 1; d >>= 1) x = add(x, shfl_xor(x, d));
+    return x;
+  } else {
+    constexpr int H = N / 2;
+    const bool upper = (lane & OFF) != 0;
+    T w[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const T mine = upper ? v[k + H] : v[k];
+      const T other = upper ? v[k] : v[k + H];
+      w[k] = add(mine, shfl_xor(other, OFF));
+    }
+    return warp_reduce_scatter_step<H, OFF / 2>(w, lane);
+  }
+}
+
+// Reduce-scatter of N per-lane values across the warp (N a power of two <= 32):
+// returns the 32-lane total of value index lane / (32 / N) -- N + 5 - log2(N)
+// shuffles instead of 5N for N separate warp sums.
+template <int N, typename T>
+__device__ __forceinline__ T warp_reduce_scatter(T (&v)[N], int lane) {
+  static_assert(N >= 1 && N <= 32 && (N & (N - 1)) == 0, "power of two");
+  if constexpr (N == 1) {
+    return warp_sum(v[0]);
+  } else {
+    // halving steps: offsets 16, 8, ... while more than one value remains
+    constexpr int H = N / 2;
+    const bool upper = (lane & 16) != 0;
+    T w[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const T mine = upper ? v[k + H] : v[k];
+      const T other = upper ? v[k] : v[k + H];
+      w[k] = add(mine, shfl_xor(other, 16));
+    }
+    return warp_reduce_scatter_step<H, 8>(w, lane);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // phase 1
 template <typename InT, bool SQ>
@@ -262,6 +306,28 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
   LocSq csq[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) { cs[k] = Loc(0); csq[k] = LocSq(0); }
+  // u8: bytes are summed two per 32-bit register (16-bit halves, exact for
+  // <= 257 rows) and flushed into cs every 256 rows
+  constexpr bool kPacked = sizeof(InT) == 1;
+  constexpr int NWD = Pack<InT>::NW;
+  uint32_t pk_lo[kPacked ? NWD : 1], pk_hi[kPacked ? NWD : 1];
+#pragma unroll
+  for (int i = 0; i < (kPacked ? NWD : 1); ++i) { pk_lo[i] = 0u; pk_hi[i] = 0u; }
+  int since_flush = 0;
+  auto flush = [&]() {
+    if constexpr (kPacked) {
+#pragma unroll
+      for (int i = 0; i < NWD; ++i) {
+        cs[4 * i + 0] = add(cs[4 * i + 0], (Loc)(pk_lo[i] & 0xFFFFu));
+        cs[4 * i + 2] = add(cs[4 * i + 2], (Loc)(pk_lo[i] >> 16));
+        cs[4 * i + 1] = add(cs[4 * i + 1], (Loc)(pk_hi[i] & 0xFFFFu));
+        cs[4 * i + 3] = add(cs[4 * i + 3], (Loc)(pk_hi[i] >> 16));
+        pk_lo[i] = 0u;
+        pk_hi[i] = 0u;
+      }
+    }
+    since_flush = 0;
+  };
 
   for (int b = 0; b < nblk; ++b) {
     const int s = b & 1;
@@ -273,28 +339,48 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
                            (int)min64(RB, k1 - rn), j0, lane);
     }
     mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
-    Acc rtot = Acc(0), rtot_sq = Acc(0);  // lane r keeps the total of row r
-    for (int r = 0; r < nr; ++r) {
-      uint32_t o[Pack<InT>::NW];
-      lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
+    Loc part[RB];      // lane partial of each staged row
+    LocSq part_sq[RB];
 #pragma unroll
-      for (int k = 0; k < E; ++k) cs[k] = add(cs[k], conv<Loc>(elem<InT>(o, k)));
-      const Loc rs = warp_sum(lane_total<InT>(o));
-      if (lane == r) rtot = (Acc)rs;
-      if constexpr (SQ) {
+    for (int r = 0; r < RB; ++r) {
+      part[r] = Loc(0);
+      part_sq[r] = LocSq(0);
+      if (r < nr) {
+        uint32_t o[NWD];
+        lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
+        part[r] = lane_total<InT>(o);
+        if constexpr (kPacked) {
 #pragma unroll
-        for (int k = 0; k < E; ++k) csq[k] = add(csq[k], convsq<LocSq>(elem<InT>(o, k)));
-        const LocSq rq = warp_sum(lane_total_sq<InT>(o));
-        if (lane == r) rtot_sq = (Acc)rq;
+          for (int i = 0; i < NWD; ++i) {
+            pk_lo[i] += o[i] & 0x00FF00FFu;
+            pk_hi[i] += (o[i] >> 8) & 0x00FF00FFu;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k) cs[k] = add(cs[k], conv<Loc>(elem<InT>(o, k)));
+        }
+        if constexpr (SQ) {
+          part_sq[r] = lane_total_sq<InT>(o);
+#pragma unroll
+          for (int k = 0; k < E; ++k) csq[k] = add(csq[k], convsq<LocSq>(elem<InT>(o, k)));
+        }
+        nf |= any_nonfinite<InT>(o);
       }
-      nf |= any_nonfinite<InT>(o);
     }
-    if (lane < nr) {
-      rowtot[(int64_t)J * PR + r0 + lane] = rtot;
-      if constexpr (SQ) rowtot_sq[(int64_t)J * PR + r0 + lane] = rtot_sq;
+    since_flush += RB;
+    if (since_flush >= 256) flush();
+    // row totals: lane l ends with the total of row l / (32 / RB)
+    const Loc rs = warp_reduce_scatter<RB>(part, lane);
+    const int myrow = lane / (32 / RB);
+    const bool writer = (lane % (32 / RB)) == 0 && myrow < nr;
+    if (writer) rowtot[(r0 + myrow) * nJ + J] = (Acc)rs;
+    if constexpr (SQ) {
+      const LocSq rq = warp_reduce_scatter<RB>(part_sq, lane);
+      if (writer) rowtot_sq[(r0 + myrow) * nJ + J] = (Acc)rq;
     }
     __syncwarp();  // stage s fully read before it is refilled
   }
+  flush();
 
   // strip-local prefix of the segment's column totals
   Acc run = Acc(0), runq = Acc(0);
@@ -319,41 +405,69 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
 }
 
 // ---------------------------------------------------------------------------
-// phase 2a: left carries (exclusive scan across strips), in place.  Loads are
-// batched so each thread keeps several independent requests in flight.
+// phase 2a: left carries (exclusive scan across strips), in place, one warp
+// per table row over the row-major [PR][nJ] row-total layout.
 template <typename Acc>
-__global__ void sat_rowcarry_kernel(Acc* __restrict__ rowtot, int nJ, int64_t PR) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kThreads)
+sat_rowcarry_kernel(Acc* __restrict__ rowtot, int nJ, int64_t PR) {
+  const int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (i >= PR) return;
-  constexpr int B = 8;
-  Acc run = Acc(0);
-  for (int J0 = 0; J0 < nJ; J0 += B) {
-    Acc v[B];
+  constexpr int MAXM = 16;  // strips per lane per pass
+  int mm = (nJ + 31) / 32;
+  if (mm > MAXM) mm = MAXM;
+  Acc* row = rowtot + i * nJ;
+  Acc carry = Acc(0);
+  for (int base = 0; base < nJ; base += 32 * mm) {
+    Acc v[MAXM];
+    Acc run = Acc(0);
 #pragma unroll
-    for (int k = 0; k < B; ++k) v[k] = (J0 + k < nJ) ? rowtot[(int64_t)(J0 + k) * PR + i] : Acc(0);
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      if (J0 + k < nJ) rowtot[(int64_t)(J0 + k) * PR + i] = run;
+    for (int k = 0; k < MAXM; ++k) {
+      const int J = base + lane * mm + k;
+      v[k] = (k < mm && J < nJ) ? row[J] : Acc(0);
       run = add(run, v[k]);
     }
+    const Acc incl = warp_incl_scan(run, lane);
+    Acc acc = add(carry, sub(incl, run));
+#pragma unroll
+    for (int k = 0; k < MAXM; ++k) {
+      const int J = base + lane * mm + k;
+      if (k < mm && J < nJ) { row[J] = acc; acc = add(acc, v[k]); }
+    }
+    carry = add(carry, __shfl_sync(0xffffffffu, incl, 31));
   }
 }
 
-// phase 2a': per (segment, strip) sum of left carries, deterministic tree.
+// phase 2a': per (segment, strip) sum of left carries: CTA (K, 32-strip group),
+// warp w sums rows k0+w, k0+w+8, ... with lanes over strips (coalesced), then a
+// fixed-order combine of the 8 warp partials.
 template <typename Acc>
 __global__ void __launch_bounds__(kThreads)
 sat_segsum_kernel(const Acc* __restrict__ rl, Acc* __restrict__ srl, int nJ, int64_t PR, int64_t SR) {
-  __shared__ Acc sw[kThreads / 32];
-  const int J = blockIdx.x, K = blockIdx.y;
+  __shared__ Acc part[kThreads / 32][32];
+  const int K = blockIdx.x;
+  const int J = blockIdx.y * 32 + (threadIdx.x & 31);
+  const int warp = threadIdx.x >> 5;
   const int64_t k0 = (int64_t)K * SR, k1 = min(k0 + SR, PR);
-  Acc s = Acc(0);
-  for (int64_t i = k0 + threadIdx.x; i < k1; i += kThreads) s = add(s, rl[(int64_t)J * PR + i]);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  Acc sacc = Acc(0);
+  if (J < nJ) {
+    constexpr int B = 8;
+    for (int64_t i0 = k0 + warp; i0 < k1; i0 += (int64_t)(kThreads / 32) * B) {
+      Acc v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int64_t i = i0 + (int64_t)u * (kThreads / 32);
+        v[u] = i < k1 ? rl[i * nJ + J] : Acc(0);
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) sacc = add(sacc, v[u]);
+    }
+  }
+  part[warp][threadIdx.x & 31] = sacc;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0 && J < nJ) {
     Acc t = Acc(0);
-    for (int w = 0; w < kThreads / 32; ++w) t = add(t, sw[w]);
+    for (int w = 0; w < kThreads / 32; ++w) t = add(t, part[w][threadIdx.x]);
     srl[(int64_t)K * nJ + J] = t;
   }
 }
@@ -462,8 +576,8 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
     }
     Acc rlv = Acc(0), rlqv = Acc(0);  // lane r: left carry of row r
     if (lane < nr) {
-      rlv = rl[(int64_t)J * PR + r0 + lane];
-      if constexpr (SQ) rlqv = rl_sq[(int64_t)J * PR + r0 + lane];
+      rlv = rl[(r0 + lane) * nJ + J];
+      if constexpr (SQ) rlqv = rl_sq[(r0 + lane) * nJ + J];
     }
     mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
     for (int r = 0; r < nr; ++r) {
@@ -546,18 +660,18 @@ cudaError_t launch_sat_prepare_t(const void* in, int64_t R, int64_t C, int64_t i
   Acc* srl = w + p.off_srl;
   Acc* srl_sq = SQ ? w + p.off_srl_sq : nullptr;
   const InT* x = reinterpret_cast<const InT*>(in);
-  dim3 grid(p.nJ, p.nK);
   const int tb = (int)(((int64_t)p.nJ * p.nK + kWarpsPerCta - 1) / kWarpsPerCta);
   const int smem = (int)(sizeof(WarpStage<InT>) * kWarpsPerCta);
   cudaError_t e = cudaFuncSetAttribute(sat_reduce_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   sat_reduce_kernel<InT, SQ><<<tb, kThreads, smem, st>>>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ,
                                                       p.nK, nonfinite);
-  const int nb_rows = (int)((p.PR + kThreads - 1) / kThreads);
+  const int nb_rows = (int)((p.PR + kThreads / 32 - 1) / (kThreads / 32));
   sat_rowcarry_kernel<Acc><<<nb_rows, kThreads, 0, st>>>(rowtot, p.nJ, p.PR);
   if (SQ) sat_rowcarry_kernel<Acc><<<nb_rows, kThreads, 0, st>>>(rowtot_sq, p.nJ, p.PR);
-  sat_segsum_kernel<Acc><<<grid, kThreads, 0, st>>>(rowtot, srl, p.nJ, p.PR, p.SR);
-  if (SQ) sat_segsum_kernel<Acc><<<grid, kThreads, 0, st>>>(rowtot_sq, srl_sq, p.nJ, p.PR, p.SR);
+  const dim3 sgrid(p.nK, (p.nJ + 31) / 32);
+  sat_segsum_kernel<Acc><<<sgrid, kThreads, 0, st>>>(rowtot, srl, p.nJ, p.PR, p.SR);
+  if (SQ) sat_segsum_kernel<Acc><<<sgrid, kThreads, 0, st>>>(rowtot_sq, srl_sq, p.nJ, p.PR, p.SR);
   const int nb_cols = (int)((p.PC + kThreads - 1) / kThreads);
   sat_topcarry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp, srl, reinterpret_cast<Acc*>(totals), p.nK, p.nJ, p.PC, p.TW);
   if (SQ) sat_topcarry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp_sq, srl_sq, reinterpret_cast<Acc*>(totals_sq), p.nK, p.nJ, p.PC, p.TW);
