@@ -1,0 +1,147 @@
+"""GPU parity at BASELINE.json sizes (C1-C5) against hashes of the reference's own
+outputs (tests/golden/make_golden.py) plus size-independent properties where
+the reference cannot run whole (C5 is compared band by band: band results are
+bit-identical to the whole-image result because table offsets cancel)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import digest
+from oracle import satsweep_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2410_16291_b200 import _lib, build_ext
+
+    build_ext.build()
+    _lib.load()
+    import paper_2410_16291_b200 as mod
+
+    return mod
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+
+    return torch.device("cuda", 0)
+
+
+def host(t, dt):
+    from paper_2410_16291_b200 import _device
+
+    return _device.to_host(t, dt)
+
+
+def to_dev(a, dev):
+    from paper_2410_16291_b200 import _device
+
+    return _device.to_device(a, dev)
+
+
+@pytest.mark.parametrize("pipe", ["table", "fused"])
+def test_c1(sb, hashes, pipe):
+    from paper_2410_16291_b200 import synthetic
+
+    got = sb.swa(synthetic.c1(), 50, "sum", pipeline=pipe)
+    assert digest(got) == hashes["C1_sum_w50"]
+
+
+@pytest.mark.parametrize("pipe", ["table", "fused"])
+def test_c2_int32(sb, hashes, dev, pipe):
+    """int32 Thomas-process raster: sum and mean in one pass; same values as the reference on the u16 cast."""
+    from paper_2410_16291_b200 import synthetic
+
+    x = synthetic.c2()
+    res = sb.swa_stats(to_dev(x, dev), 100, ("sum", "mean"), pipeline=pipe)
+    s = host(res["sum"], np.int64)
+    assert digest(s.view(np.uint64)) == hashes["C2_sum_w100"]
+    assert digest(host(res["mean"], np.float64)) == hashes["C2_mean_w100"]
+
+
+@pytest.mark.parametrize("pipe", ["table", "fused"])
+def test_c3_multi_window(sb, hashes, dev, pipe):
+    from paper_2410_16291_b200 import synthetic
+
+    x = to_dev(synthetic.c3(), dev)
+    outs = sb.multi_window(x, [25, 50, 100, 200, 400], "sum", pipeline=pipe)
+    for w, o in zip((25, 50, 100, 200, 400), outs):
+        assert digest(host(o, np.uint64)) == hashes[f"C3_sum_w{w}"], w
+        del o
+
+
+def test_c4_float(sb, hashes, golden, dev):
+    """f32 lognormal: mean/std within rtol 1e-6 of the reference on sampled rows, plus properties."""
+    from paper_2410_16291_b200 import synthetic
+
+    x = synthetic.c4()
+    res = sb.swa_stats(to_dev(x, dev), 64, ("mean", "std"), pipeline="table")
+    rows = golden["C4_rows"]
+    for stat in ("mean", "std"):
+        got = host(res[stat][rows.tolist()], np.float64)
+        np.testing.assert_allclose(got, golden[f"C4_{stat}_rows"], rtol=1e-6, atol=0)
+    # properties at full size: std >= 0, mean within [min, max] of the data
+    import torch
+
+    assert bool((res["std"] >= 0).all())
+    assert float(res["mean"].min()) >= float(x.min()) - 1e-9
+    assert float(res["mean"].max()) <= float(x.max()) + 1e-9
+    # spot rows against the oracle on the matching input band
+    for i in (5, 7777, 19936):
+        band = x[i:i + 64]
+        for stat in ("mean", "std"):
+            ref = O.swa(band, 64, stat)[0]
+            np.testing.assert_allclose(host(res[stat][i], np.float64), ref, rtol=1e-6)
+    del res
+    torch.cuda.empty_cache()
+
+
+def test_c4_fused_vs_table(sb, dev):
+    from paper_2410_16291_b200 import synthetic
+
+    x = to_dev(synthetic.c4(4000, 24000), dev)
+    a = sb.swa_stats(x, 64, ("mean", "std"), pipeline="table")
+    b = sb.swa_stats(x, 64, ("mean", "std"), pipeline="fused")
+    for s in ("mean", "std"):
+        np.testing.assert_allclose(host(b[s], np.float64), host(a[s], np.float64), rtol=1e-9)
+
+
+@pytest.mark.parametrize("band", [(0, 2048), (34000, 34512), (69745 - 512, 69745)])
+def test_c5_bands(sb, hashes, dev, band):
+    from paper_2410_16291_b200 import synthetic
+
+    lo, hi = band
+    x = to_dev(synthetic.c5(lo, hi + 255), dev)
+    for pipe in ("table", "fused"):
+        got = host(sb.swa(x, 256, "sum", pipeline=pipe), np.uint64)
+        assert digest(got) == hashes[f"C5_sum_w256_rows{lo}_{hi}"], pipe
+
+
+def test_c5_full_image(sb, hashes, dev):
+    """Whole 70,000 x 85,000 raster on one GPU: reference-hashed bands of the full result,
+    random rows against the oracle, and table == fused."""
+    import torch
+
+    from paper_2410_16291_b200 import synthetic
+
+    x = to_dev(synthetic.c5(), dev)
+    out = sb.swa(x, 256, "sum", pipeline="table")
+    assert tuple(out.shape) == (69745, 84745)
+    for lo, hi in ((0, 2048), (34000, 34512), (69745 - 512, 69745)):
+        assert digest(host(out[lo:hi], np.uint64)) == hashes[f"C5_sum_w256_rows{lo}_{hi}"]
+    rng = np.random.default_rng(5)
+    for i in rng.integers(0, 69745, size=3).tolist():
+        band = host(x[i:i + 256], np.uint8)
+        np.testing.assert_array_equal(host(out[i], np.uint64), O.swa(band, 256, "sum")[0])
+    fused = sb.swa(x, 256, "sum", pipeline="fused")
+    assert bool(torch.equal(fused, out))
+    del out, fused, x
+    torch.cuda.empty_cache()
