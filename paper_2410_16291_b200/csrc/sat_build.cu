@@ -31,6 +31,7 @@
 
 #include "ssb_async.cuh"
 #include "ssb_common.cuh"
+#include "ssb_stage.cuh"
 
 namespace ssb {
 
@@ -46,7 +47,6 @@ struct Geo {
   static constexpr int CPT = TW / kThreads;          // columns per thread in column passes
 };
 
-constexpr int kNoRow = INT_MIN;
 
 // ---- TMA row staging ----------------------------------------------------------
 // Warp 0 stages table rows [r0, r0+nr) x table cols [j0, j0+TW) of the padded
@@ -64,38 +64,11 @@ __device__ __forceinline__ void stage_issue(unsigned char* stage, int* offs, uin
   const int64_t c_hi = (j0 - 1 + G::TW) < C ? (j0 - 1 + G::TW) : C;
   const int64_t ir = r0 + lane - 1;
   const bool has = lane < nr && ir >= 0 && ir < R && c_hi > c_lo;
-  const char* a = nullptr;
-  const char* b = nullptr;
-  if (has) {
-    const char* rowp = base + ir * in_ld * G::ES;
-    const char* lo = rowp + c_lo * G::ES;
-    const char* hi = rowp + c_hi * G::ES;
-    a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15));
-    b = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15));
-    if (b > end_valid) {  // never read past the raster: copy the tail bytes by hand
-      b = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(end_valid) & ~uintptr_t(15));
-      if (b < a) b = a;
-      unsigned char* dst = stage + lane * G::ROWB + 16;
-      for (const char* p = b; p < hi; ++p) dst[p - a] = (unsigned char)__ldg(reinterpret_cast<const char*>(p));
-    }
-    offs[lane] = (int)(rowp - a);
-  } else if (lane < RB) {
-    offs[lane] = kNoRow;
-  }
-  uint32_t bytes = has ? (uint32_t)(b - a) : 0u;
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, d);
-  fence_proxy_async();
-  __syncwarp();
-  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
-  __syncwarp();
-  if (has && b > a) bulk_g2s(stage + lane * G::ROWB + 16, a, (uint32_t)(b - a), bar);
-}
-
-template <int NO, int SW>
-__device__ __forceinline__ void shift_words(const uint32_t* w, uint32_t* o, int sb) {
-#pragma unroll
-  for (int k = 0; k < NO; ++k) o[k] = __funnelshift_r(w[k + SW], w[k + SW + 1], sb);
+  RowSpan sp;
+  unsigned char* dst = stage + lane * G::ROWB;
+  if (has) sp = row_span(base + ir * in_ld * G::ES, c_lo, c_hi, G::ES, end_valid, dst);
+  if (lane < RB) offs[lane] = has ? sp.off : kNoRow;
+  warp_issue(sp, has, dst, bar, lane);
 }
 
 // Lane's E consecutive elements starting at image column c0 of staged row r,
@@ -106,50 +79,10 @@ template <typename InT> struct Pack {
 };
 
 template <typename InT>
-__device__ __forceinline__ InT elem(const uint32_t* o, int k) {
-  if constexpr (sizeof(InT) == 1) return (InT)(o[k >> 2] >> (8 * (k & 3)));
-  else if constexpr (sizeof(InT) == 2) return (InT)(o[k >> 1] >> (16 * (k & 1)));
-  else { InT v; memcpy(&v, &o[k], 4); return v; }
-}
-
-template <typename InT>
-__device__ __forceinline__ void clear_elem(uint32_t* o, int k) {
-  if constexpr (sizeof(InT) == 1) o[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
-  else if constexpr (sizeof(InT) == 2) o[k >> 1] &= ~(0xFFFFu << (16 * (k & 1)));
-  else o[k] = 0u;
-}
-
-template <typename InT>
 __device__ __forceinline__ void lane_words(const unsigned char* stage, const int* offs, int r, int64_t c0, int64_t C,
                                            uint32_t (&o)[Pack<InT>::NW]) {
   using G = Geo<InT>;
-  constexpr int NC = G::LB / 16 + 1, NO = Pack<InT>::NW;
-  const int off = offs[r];
-  if (off == kNoRow) {
-#pragma unroll
-    for (int k = 0; k < NO; ++k) o[k] = 0u;
-    return;
-  }
-  const int Q = 16 + off + (int)(c0 * G::ES);
-  const uint4* p = reinterpret_cast<const uint4*>(stage + r * G::ROWB + (Q & ~15));
-  uint32_t w[NC * 4];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const uint4 v = p[c];
-    w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
-  }
-  const int s = Q & 15, sb = (s & 3) * 8;
-  switch (s >> 2) {  // warp-uniform: lanes differ by multiples of 16 bytes
-    case 0: shift_words<NO, 0>(w, o, sb); break;
-    case 1: shift_words<NO, 1>(w, o, sb); break;
-    case 2: shift_words<NO, 2>(w, o, sb); break;
-    default: shift_words<NO, 3>(w, o, sb); break;
-  }
-  if (c0 < 0 || c0 + G::E > C) {
-#pragma unroll
-    for (int k = 0; k < G::E; ++k)
-      if (c0 + k < 0 || c0 + k >= C) clear_elem<InT>(o, k);
-  }
+  lane_elems_packed<InT, G::E>(stage + r * G::ROWB, offs[r], c0, C, o);
 }
 
 // sum of the lane's elements in Loc / of their squares in LocSq

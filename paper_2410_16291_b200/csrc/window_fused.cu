@@ -15,7 +15,10 @@
 // Integer sums use modular arithmetic of the narrowest width that holds the
 // final window sum (u32 for u8 while w^2*255 < 2^32), so intermediate prefix
 // sums may wrap without affecting the result.  f32 input uses double.
+#include <cstdlib>
+
 #include "ssb_common.cuh"
+#include "ssb_stage.cuh"
 
 namespace ssb {
 
@@ -231,6 +234,225 @@ cudaError_t launch_fused_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Strip kernel (default).  Every warp owns one output-column strip of TWo = NV
+// - w + 1 columns (NV = 32 E image columns incl. the w-1 halo) and one segment
+// of output rows, and sweeps it top to bottom on its own 2-deep TMA ring
+// (rows r and r-w staged per step, ssb_stage.cuh).  Lane l keeps the vertical
+// sums V of image columns [l E, l E + E) in registers -- for uint8 with
+// w <= 256 two columns per register as 16-bit halves (V <= 65280).  Per
+// finished row the lane-serial prefix + one warp scan give P, written to a
+// per-warp smem buffer with one pad word per lane block (column t at word
+// t + t / E: conflict-free for the lane-contiguous writes because E + 1 is odd,
+// and nearly so for the lane-consecutive reads), so out[j] = P[j+w] - P[j] is
+// read and stored by consecutive lanes (coalesced 8-byte stores).  No CTA
+// barrier anywhere.
+constexpr int kStripWarps = 4;  // warps per CTA
+
+template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ>
+struct StripSmem {
+  static constexpr int NV = 32 * E;
+  static constexpr int ROWB = NV * (int)sizeof(InT) + 48;
+  alignas(16) unsigned char stage[2][2 * RB][ROWB];
+  int offs[2][2 * RB];
+  uint64_t bar[2];
+  VT p[NV + 32];                  // inclusive prefix of column t at word t + t / E
+  VQ pq[SQ ? NV + 32 : 1];
+};
+
+template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ, bool PACK>
+__global__ void __launch_bounds__(32 * kStripWarps, 3)
+fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeInt fi, int nJ, int nK,
+                   int* __restrict__ nonfinite) {
+  using SM = StripSmem<InT, E, RB, VT, VQ, SQ>;
+  constexpr int NV = SM::NV, ES = (int)sizeof(InT), NW = E * ES / 4;
+  constexpr bool kFloat = Elem<InT>::kFloat;
+  static_assert(!PACK || (ES == 1 && sizeof(VT) == 4), "packed vertical sums are for uint8");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SM& sm = reinterpret_cast<SM*>(smem_raw)[warp];
+  const int t = blockIdx.x * kStripWarps + warp;
+  if (t >= nJ * nK) return;
+  const int J = t % nJ, K = t / nJ;
+  const int w = g.w;
+  const int64_t oc0 = (int64_t)J * g.two;
+  const int nout = (int)min64(g.two, g.out_c - oc0);
+  const int64_t or0 = (int64_t)K * g.sro, or1 = min64(or0 + g.sro, g.out_r);
+  if (nout <= 0 || or0 >= or1) return;
+  const int64_t r_beg = or0, r_end = or1 + w - 1;  // input rows of this segment
+  const int nblk = (int)((r_end - r_beg + RB - 1) / RB);
+  const int64_t c_lo = oc0, c_hi = min64(oc0 + NV, g.C);
+  const int64_t c0 = oc0 + lane * E;
+  const char* base = reinterpret_cast<const char*>(in);
+  const char* end_valid = base + ((g.R - 1) * g.in_ld + g.C) * ES;
+  if (lane == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  // lane q < RB stages new row rb+q; lane RB+q stages old row rb+q-w
+  auto issue = [&](int b, int s) {
+    const int64_t rb = r_beg + (int64_t)b * RB;
+    const int q = lane % RB;
+    const bool old = lane >= RB;
+    const int64_t r = rb + q - (old ? w : 0);
+    const bool has = lane < 2 * RB && rb + q < r_end && (!old || rb + q - w >= r_beg);
+    unsigned char* dst = sm.stage[s][lane < 2 * RB ? lane : 0];
+    RowSpan sp;
+    if (has) sp = row_span(base + r * g.in_ld * ES, c_lo, c_hi, ES, end_valid, dst);
+    if (lane < 2 * RB) sm.offs[s][lane] = has ? sp.off : kNoRow;
+    warp_issue(sp, has, dst, &sm.bar[s], lane);
+  };
+  issue(0, 0);
+
+  constexpr int NVR = PACK ? E / 2 : E;  // registers holding V
+  VT V[NVR];
+  VQ Vq[E];
+#pragma unroll
+  for (int k = 0; k < NVR; ++k) V[k] = VT(0);
+#pragma unroll
+  for (int k = 0; k < E; ++k) Vq[k] = VQ(0);
+  bool nf = false;
+  const int wbase = lane * (E + 1);  // word of this lane's first column
+
+  for (int b = 0; b < nblk; ++b) {
+    const int s = b & 1;
+    if (b + 1 < nblk) issue(b + 1, s ^ 1);
+    mbar_wait(&sm.bar[s], (uint32_t)((b >> 1) & 1));
+    const int64_t rb = r_beg + (int64_t)b * RB;
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int64_t r = rb + q;
+      if (r >= r_end) break;
+      uint32_t on[NW], oo[NW];
+      lane_elems_packed<InT, E>(sm.stage[s][q], sm.offs[s][q], c0, g.C, on);
+      lane_elems_packed<InT, E>(sm.stage[s][RB + q], sm.offs[s][RB + q], c0, g.C, oo);  // zeros until r >= r_beg + w
+      if constexpr (PACK) {
+        // V[2i] holds columns 4i, 4i+2 and V[2i+1] columns 4i+1, 4i+3 (16-bit halves)
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          V[2 * i] += (on[i] & 0x00FF00FFu);
+          V[2 * i] -= (oo[i] & 0x00FF00FFu);
+          V[2 * i + 1] += ((on[i] >> 8) & 0x00FF00FFu);
+          V[2 * i + 1] -= ((oo[i] >> 8) & 0x00FF00FFu);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const InT xn = elem<InT>(on, k), xo = elem<InT>(oo, k);
+          V[k] = sub(add(V[k], tv<VT>(xn)), tv<VT>(xo));
+          if constexpr (kFloat) nf |= is_nonfinite(xn);
+        }
+      }
+      if constexpr (SQ) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const InT xn = elem<InT>(on, k), xo = elem<InT>(oo, k);
+          if constexpr (kFloat) Vq[k] = sub(add(Vq[k], __dmul_rn((double)xn, (double)xn)), __dmul_rn((double)xo, (double)xo));
+          else Vq[k] = sub(add(Vq[k], tv<VQ>(xn) * tv<VQ>(xn)), tv<VQ>(xo) * tv<VQ>(xo));
+        }
+      }
+      if (r < r_beg + w - 1) continue;  // window not yet complete
+      const int64_t i = r - (w - 1);
+      {
+        auto vcol = [&](int k) -> VT {
+          if constexpr (PACK) {
+            const uint32_t pair = V[2 * (k >> 2) + (k & 1)];
+            return (VT)((k & 2) ? (pair >> 16) : (pair & 0xFFFFu));
+          } else {
+            return V[k];
+          }
+        };
+        VT tot = VT(0);
+#pragma unroll
+        for (int k = 0; k < E; ++k) tot = add(tot, vcol(k));
+        VT run = sub(warp_incl_scan(tot, lane), tot);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          run = add(run, vcol(k));
+          sm.p[wbase + k] = run;
+        }
+      }
+      if constexpr (SQ) {
+        VQ tot = VQ(0);
+#pragma unroll
+        for (int k = 0; k < E; ++k) tot = add(tot, Vq[k]);
+        VQ run = sub(warp_incl_scan(tot, lane), tot);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          run = add(run, Vq[k]);
+          sm.pq[wbase + k] = run;
+        }
+      }
+      __syncwarp();
+      const int64_t obase = i * o.ld + oc0;
+      for (int j = lane; j < nout; j += 32) {
+        const int ta = j - 1, tb = j + w - 1;  // inclusive prefixes P[j] = Pin[j-1], P[j+w] = Pin[j+w-1]
+        const int qa = ta + ta / E, qb = tb + tb / E;
+        const VT pa = (j == 0) ? VT(0) : sm.p[qa];
+        const VT sv = sub(sm.p[qb], pa);
+        VQ qv = VQ(0);
+        if constexpr (SQ) qv = sub(sm.pq[qb], (j == 0) ? VQ(0) : sm.pq[qa]);
+        if constexpr (kFloat) {
+          if (g.mask & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + obase + j, (double)sv);
+          if (g.mask & ST_MEAN) st_cs(o.mean + obase + j, fin_mean_f((double)sv, fi.dn));
+          if (g.mask & ST_STD) st_cs(o.std_ + obase + j, fin_std_f((double)sv, (double)qv, fi.dn));
+        } else {
+          uint64_t s64, q64 = 0;
+          if constexpr (sizeof(VT) == 4) s64 = (uint64_t)(uint32_t)sv; else s64 = (uint64_t)sv;
+          if constexpr (SQ) { if constexpr (sizeof(VQ) == 4) q64 = (uint64_t)(uint32_t)qv; else q64 = (uint64_t)qv; }
+          if (g.mask & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + obase + j, s64);
+          if (g.mask & ST_MEAN) st_cs(o.mean + obase + j, fin_mean_int(s64, fi));
+          if (g.mask & ST_STD) st_cs(o.std_ + obase + j, fin_std_int(s64, q64, fi));
+        }
+      }
+      __syncwarp();
+    }
+    __syncwarp();  // stage s fully read before it is refilled
+  }
+  if (nf && nonfinite) atomicOr(nonfinite, 1);
+}
+
+template <typename InT, int E, typename VT, typename VQ, bool SQ, bool PACK>
+cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK_override,
+                           cudaStream_t st) {
+  constexpr int ROWB = 32 * E * (int)sizeof(InT) + 48;
+  constexpr int RB = ROWB <= 1100 ? 2 : 1;
+  using SM = StripSmem<InT, E, RB, VT, VQ, SQ>;
+  g.two = SM::NV - g.w + 1;
+  const int nJ = (int)((g.out_c + g.two - 1) / g.two);
+  int64_t nK = nK_override > 0 ? nK_override : (int64_t)(2 * kNumSMs * 12 + nJ - 1) / nJ;
+  if (nK > g.out_r) nK = g.out_r;
+  if (nK < 1) nK = 1;
+  g.sro = (g.out_r + nK - 1) / nK;
+  nK = (g.out_r + g.sro - 1) / g.sro;
+  auto kfn = fused_strip_kernel<InT, E, RB, VT, VQ, SQ, PACK>;
+  const size_t smem = sizeof(SM) * kStripWarps;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t warps = (int64_t)nJ * nK;
+  const int blocks = (int)((warps + kStripWarps - 1) / kStripWarps);
+  kfn<<<blocks, 32 * kStripWarps, smem, st>>>(reinterpret_cast<const InT*>(in), g, o, fi, nJ, (int)nK, nonfinite);
+  note_launch(1);
+  return cudaGetLastError();
+}
+
+// uint8 with packed vertical sums (w <= 256, no squares): 64 bytes of raster
+// per lane and row (2048-column strips); otherwise 32 bytes per lane.  Falls
+// back to the CTA kernel below when fewer than 64 outputs per strip remain.
+template <typename InT, typename VT, typename VQ, bool SQ>
+bool launch_strip(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK, cudaStream_t st,
+                  cudaError_t& err) {
+  constexpr int E1 = 32 / (int)sizeof(InT);
+  if constexpr (sizeof(InT) == 1 && sizeof(VT) == 4 && !SQ) {
+    if (g.w <= 256) { err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, true>(in, g, o, fi, nonfinite, nK, st); return true; }
+  }
+  if (32 * E1 - g.w + 1 < 64) return false;
+  err = launch_strip_t<InT, E1, VT, VQ, SQ, false>(in, g, o, fi, nonfinite, nK, st);
+  return true;
+}
+
 // rows per group: keep the G x E snapshot registers at <= 64 32-bit registers
 template <typename VT, typename VQ, bool SQ, int E>
 constexpr int fused_group() {
@@ -241,6 +463,11 @@ constexpr int fused_group() {
 
 template <typename InT, typename VT, typename VQ, bool SQ>
 cudaError_t launch_fused_e(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK, cudaStream_t st) {
+  const char* env = getenv("SSB_FUSED_PATH");  // tuning: "cta" forces the CTA kernel
+  if (!(env && env[0] == 'c')) {
+    cudaError_t err = cudaSuccess;
+    if (launch_strip<InT, VT, VQ, SQ>(in, g, o, fi, nonfinite, nK, st, err)) return err;
+  }
   if (g.w <= 256) return launch_fused_t<InT, VT, VQ, SQ, 4, fused_group<VT, VQ, SQ, 4>()>(in, g, o, fi, nonfinite, nK, st);
   if (g.w <= 1024) return launch_fused_t<InT, VT, VQ, SQ, 8, fused_group<VT, VQ, SQ, 8>()>(in, g, o, fi, nonfinite, nK, st);
   return launch_fused_t<InT, VT, VQ, SQ, 16, fused_group<VT, VQ, SQ, 16>()>(in, g, o, fi, nonfinite, nK, st);
