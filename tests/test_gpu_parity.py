@@ -276,3 +276,27 @@ def test_host_streaming_bands(sb):
                         np.testing.assert_allclose(many[k], one[k], rtol=1e-9, atol=1e-9)
                     else:
                         np.testing.assert_array_equal(many[k], one[k])
+
+
+def test_reference_seams(sb, rng):
+    """seams.builder / seams.sweep behind the reference's builder/sweep signatures
+    (integral.py:166-189), driven like _sats_for_stat/_finalize_from_sats would."""
+    from types import SimpleNamespace
+
+    from paper_2410_16291_b200 import seams
+
+    for kind in KINDS:
+        v = random_values(rng, 97, 131, kind)
+        img = SimpleNamespace(values=v, elem_kind=None)
+        win = SimpleNamespace(w=9, stride=2)
+        sat = seams.builder(img, False)
+        np.testing.assert_array_equal(sat.table, O.build_table(v)) if kind != "f32" else \
+            np.testing.assert_allclose(sat.table, O.build_table(v), rtol=1e-12)
+        out_r, out_c = O.out_shape(97, 131, 9, 2)
+        ref = O.corner_sums(O.build_table(v), 9, 2, out_r, out_c)
+        for table in (sat, SimpleNamespace(table=O.build_table(v))):
+            got = seams.sweep(table, win, out_r, out_c)
+            if kind == "f32":
+                np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-9)
+            else:
+                np.testing.assert_array_equal(got, ref)
