@@ -247,6 +247,8 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
 #pragma unroll
   for (int i = 0; i < (kPacked ? NWD : 1); ++i) { pk_lo[i] = 0u; pk_hi[i] = 0u; }
   int since_flush = 0;
+  const bool lane_inside = c0 >= 0 && c0 + E <= C;
+  const int qbase = 16 + (int)(c0 * G::ES);
   auto flush = [&]() {
     if constexpr (kPacked) {
 #pragma unroll
@@ -274,13 +276,17 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
     mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
     Loc part[RB];      // lane partial of each staged row
     LocSq part_sq[RB];
+    // interior blocks (all RB rows are image rows) on interior lanes (all E
+    // columns inside the image) take a check-free path
+    const bool fast = lane_inside && nr == RB && r0 >= 1 && r0 + RB - 1 <= R;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       part[r] = Loc(0);
       part_sq[r] = LocSq(0);
-      if (r < nr) {
+      if (fast || r < nr) {
         uint32_t o[NWD];
-        lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
+        if (fast) lane_bytes<G::LB>(ws.buf[s] + r * G::ROWB, qbase + ws.offs[s][r], o);
+        else lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
         part[r] = lane_total<InT>(o);
         if constexpr (kPacked) {
 #pragma unroll
