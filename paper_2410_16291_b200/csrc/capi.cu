@@ -30,6 +30,9 @@ cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_floa
                                int64_t sat_ld, int64_t w, int64_t s, int mask, WinOut o, cudaStream_t st);
 cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
                                 WinOut o, int* nonfinite, int nK, cudaStream_t st);
+cudaError_t launch_window_eval_multi(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R,
+                                     int64_t C, int64_t sat_ld, int nwin, const int64_t* ws, int mask, const WinOut* outs,
+                                     cudaStream_t st);
 constexpr int64_t kFusedMaxWindow = 3072;
 
 static std::atomic<long long> g_launches{0};
@@ -168,11 +171,40 @@ int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int
     int rc = check_window(rows, cols, windows[k], 1);
     if (rc) return rc;
   }
-  for (int k = 0; k < n_windows; ++k) {
-    int rc = ssb_window_eval(sat, sat_sq, in_dtype, rows, cols, sat_ld, windows[k], 1, stat_mask,
-                             out_sums ? out_sums[k] : nullptr, out_means ? out_means[k] : nullptr,
-                             out_stds ? out_stds[k] : nullptr, out_lds[k], stream);
-    if (rc) return rc;
+  int rc = check_stats(in_dtype, stat_mask);
+  if (rc) return rc;
+  if (!sat || sat_ld < cols + 1) return fail(SSB_EINVAL, "bad table");
+  if ((stat_mask & SSB_STD) && !sat_sq) return fail(SSB_EINVAL, "squared sums required for std dev");
+  // groups of up to 8 windows share one pass over the table
+  for (int k0 = 0; k0 < n_windows; k0 += 8) {
+    const int nk = n_windows - k0 < 8 ? n_windows - k0 : 8;
+    WinOut outs[8];
+    bool ok = true;
+    for (int k = 0; k < nk; ++k) {
+      const int kk = k0 + k;
+      outs[k] = WinOut{out_sums ? out_sums[kk] : nullptr, out_means ? out_means[kk] : nullptr,
+                       out_stds ? out_stds[kk] : nullptr, out_lds[kk]};
+      if (((stat_mask & SSB_SUM) && !outs[k].sum) || ((stat_mask & SSB_MEAN) && !outs[k].mean) ||
+          ((stat_mask & SSB_STD) && !outs[k].std_))
+        return fail(SSB_EINVAL, "missing output buffer");
+      if (out_lds[kk] < cols - windows[kk] + 1) return fail(SSB_EINVAL, "out_ld < output cols");
+    }
+    cudaError_t e = launch_window_eval_multi(sat, sat_sq, in_dtype == SSB_F32, in_dtype, rows, cols, sat_ld, nk,
+                                             windows + k0, stat_mask, outs, as_stream(stream));
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      ok = false;
+    } else if (e != cudaSuccess) {
+      return cuda_fail(e, "ssb_window_eval_multi");
+    }
+    if (!ok) {
+      for (int k = 0; k < nk; ++k) {
+        const int kk = k0 + k;
+        rc = ssb_window_eval(sat, sat_sq, in_dtype, rows, cols, sat_ld, windows[kk], 1, stat_mask, outs[k].sum,
+                             outs[k].mean, outs[k].std_, out_lds[kk], stream);
+        if (rc) return rc;
+      }
+    }
   }
   return SSB_OK;
 }

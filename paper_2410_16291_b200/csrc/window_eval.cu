@@ -220,34 +220,60 @@ inline int64_t panel_width(int64_t out_c, int64_t w, int64_t s, bool sq, int64_t
 // of KB per SM in flight without occupying load slots.
 constexpr int kTmaMaxNS = 8;  // pipeline depth (runtime, <= 8)
 
-struct TmaPlan {
-  int64_t seg;     // elements per staged row segment (even)
-  int64_t steps;   // row steps per CTA (upper bound, all panels)
-  int ntab;        // 1 (sum) or 2 (sum + squares)
-};
-
-// Work items (panel, output row, chunk) are handed out in that order by an
-// atomic ticket, so the items in flight are always a contiguous range of the
-// global order: the rows being evaluated stay a narrow band of one panel and a
-// table row fetched as a bottom corner row is still in L2 when it is needed as
-// a top corner row w rows later (a static assignment lets CTAs drift apart).
+// Work items are handed out in order by an atomic ticket, so the items in
+// flight are always a contiguous range of the global order: the rows being
+// evaluated stay a narrow band of one panel and a table row fetched as a bottom
+// corner row is still in L2 when it is needed as a top corner row w rows later
+// (a static assignment lets CTAs drift apart and doubled the table reads).
+//
+// Item = (panel p, bottom table row rb, window k, chunk c): output row
+// rb - w_k of window k.  With several windows (multi_window, integral.py:199-210)
+// all windows that use table row rb as their bottom row are evaluated back to
+// back, so every table byte comes from HBM about once for the whole window set.
 __device__ unsigned long long g_eval_tickets[256];
 
-template <typename Acc, bool SQ, int U>
+constexpr int kMaxWin = 8;
+struct MultiEval {
+  int nwin;
+  int mask;
+  int is_signed;
+  int64_t wmin, wmax, R, sat_ld;
+  int64_t pw, n_panels, cpp, cpl;       // panels of output columns (chunks of CW)
+  int64_t w[kMaxWin], out_r[kMaxWin], out_c[kMaxWin];
+  WinOut o[kMaxWin];
+  uint64_t n[kMaxWin];
+  double dn[kMaxWin];
+  unsigned char u64_ok[kMaxWin];
+};
+
+template <typename Acc> struct FinK;
+template <> struct FinK<uint64_t> {
+  __device__ static Fin<uint64_t> make(const MultiEval& m, int k) {
+    Fin<uint64_t> f{};
+    f.f.n = m.n[k]; f.f.dn = m.dn[k]; f.f.u64_ok = m.u64_ok[k] != 0; f.f.is_signed = m.is_signed != 0;
+    return f;
+  }
+};
+template <> struct FinK<double> {
+  __device__ static Fin<double> make(const MultiEval& m, int k) { return Fin<double>{m.dn[k]}; }
+};
+
+template <typename Acc, bool SQ, int U, bool MULTI>
 __global__ void __launch_bounds__(kThreads)
-window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, EvalGeom g, WinOut o, Fin<Acc> fin,
+window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, const __grid_constant__ MultiEval g,
                        int64_t seg, unsigned long long* __restrict__ ticket, int NS, int batch) {
   constexpr int NT = SQ ? 2 : 1;
-  constexpr int kTmaCW = kThreads * U;  // outputs per row step
+  constexpr int kTmaCW = kThreads * U;  // outputs per item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + kTmaMaxNS;
-  int64_t* meta = reinterpret_cast<int64_t*>(empty + kTmaMaxNS);  // [NS] item of each stage (-1: done)
+  int64_t* meta = reinterpret_cast<int64_t*>(empty + kTmaMaxNS);  // [NS] item of each stage (-1 done, -2 skip)
   Acc* buf = reinterpret_cast<Acc*>(smem_raw + 256);              // [NS][NT][2][seg]
   const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t w = g.w, ld = g.sat_ld;
-  const int64_t per_panel = g.out_r * g.cpp;
-  const int64_t total = per_panel * (g.n_panels - 1) + g.out_r * g.cpl;
+  const int64_t ld = g.sat_ld;
+  const int64_t nrb = g.R + 1 - g.wmin;  // bottom rows wmin..R
+  const int64_t per_panel = nrb * g.nwin * g.cpp;
+  const int64_t total = per_panel * (g.n_panels - 1) + nrb * g.nwin * g.cpl;
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
@@ -256,20 +282,35 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
     fence_mbar_init();
   }
   __syncthreads();
-  auto coords = [&](int64_t it, int64_t& i, int64_t& j0) {
-    const int64_t p = it / per_panel;
-    const int64_t rem = it - p * per_panel;
-    const int64_t cpp = (p == g.n_panels - 1) ? g.cpl : g.cpp;
-    i = rem / cpp;
-    j0 = p * g.pw + (rem - i * cpp) * kTmaCW;
+  // item -> (output row i, window k, first column j0); false if the item maps to
+  // no output.  32-bit arithmetic (item counts stay far below 2^31).
+  const uint32_t ppan = (uint32_t)per_panel, cppf = (uint32_t)g.cpp, cppl = (uint32_t)g.cpl;
+  auto coords = [&](int64_t it64, int64_t& i, int& k, int64_t& j0) -> bool {
+    const uint32_t it = (uint32_t)it64;
+    const uint32_t p = it / ppan;
+    const uint32_t rem = it - p * ppan;
+    const uint32_t cpp = ((int64_t)p == g.n_panels - 1) ? cppl : cppf;
+    uint32_t rb_off, c;
+    if constexpr (MULTI) {
+      const uint32_t per_row = (uint32_t)g.nwin * cpp;
+      rb_off = rem / per_row;
+      const uint32_t rem2 = rem - rb_off * per_row;
+      k = (int)(rem2 / cpp);
+      c = rem2 - (uint32_t)k * cpp;
+    } else {
+      rb_off = rem / cpp;
+      k = 0;
+      c = rem - rb_off * cpp;
+    }
+    j0 = (int64_t)p * g.pw + (int64_t)c * kTmaCW;
+    i = (int64_t)rb_off + g.wmin - g.w[k];
+    return i >= 0 && i < g.out_r[k] && j0 < g.out_c[k];
   };
   bool producing = true;
   // tickets come in batches of `batch` consecutive items (one atomic per
   // batch); the next batch is requested while the current one is issued
   int64_t cur = 0, cur_end = 0, next_b = 0;
-  if (tid == 0) {
-    next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
-  }
+  if (tid == 0) next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
   auto produce = [&](int64_t m) {  // thread 0 only
     const int s = (int)(m % NS);
     if (m >= NS) mbar_wait(&empty[s], (uint32_t)(((m / NS) - 1) & 1));
@@ -285,10 +326,17 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
       mbar_arrive_expect_tx(&full[s], 0);
       return;
     }
-    meta[s] = it;
     int64_t i, j0;
-    coords(it, i, j0);
-    int64_t len = ld - j0 < seg ? ld - j0 : seg;
+    int k;
+    if (!coords(it, i, k, j0)) {
+      meta[s] = -2;
+      mbar_arrive_expect_tx(&full[s], 0);
+      return;
+    }
+    meta[s] = it;
+    const int64_t w = g.w[k];
+    const int64_t need = (kTmaCW + w + 1) & ~int64_t(1);
+    int64_t len = ld - j0 < need ? ld - j0 : need;
     len &= ~int64_t(1);
     const uint32_t bytes = (uint32_t)(len * 8);
     fence_proxy_async();
@@ -308,9 +356,16 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
     const int s = (int)(m % NS);
     mbar_wait(&full[s], (uint32_t)((m / NS) & 1));
     const int64_t it = meta[s];
-    if (it < 0) break;
+    if (it == -1) break;
+    if (it == -2) {
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      continue;
+    }
     int64_t i, j0;
-    coords(it, i, j0);
+    int k;
+    coords(it, i, k, j0);
+    const int64_t w = g.w[k];
     const Acc* T = buf + (int64_t)s * NT * 2 * seg;
     const Acc* B = T + seg;
     Acc sv[U], qv[U];
@@ -326,11 +381,14 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    const WinOut& o = g.o[k];
+    const Fin<Acc> fin = FinK<Acc>::make(g, k);
     const int64_t base = i * o.ld + j0;
+    const int64_t oc = g.out_c[k];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + tid + kThreads * u;
-      if (j >= g.out_c) break;
+      if (j >= oc) break;
       const int64_t at = base + tid + kThreads * u;
       if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, sv[u]);
       if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(sv[u]));
@@ -339,13 +397,23 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
   }
 }
 
+// panel width (output columns, multiple of `chunk`) that keeps the w+1 table
+// rows a panel touches (both tables) within ~`budget` bytes of L2
+inline int64_t panel_width_max(int64_t out_c, int64_t wmax, bool sq, int64_t chunk, double budget) {
+  const double row_bytes = 8.0 * (sq ? 2 : 1) * (double)(wmax + 1);
+  int64_t pw = (int64_t)(budget / row_bytes);
+  pw = (pw / chunk) * chunk;
+  if (pw < chunk) pw = chunk;
+  const int64_t full = ((out_c + chunk - 1) / chunk) * chunk;
+  return pw > full ? full : pw;
+}
+
 template <typename Acc, bool SQ, int U>
-cudaError_t launch_tma_u(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, cudaStream_t st,
-                       bool& used) {
+cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m, cudaStream_t st, bool& used) {
   used = false;
   constexpr int NT = SQ ? 2 : 1;
   constexpr int64_t kTmaCW = kThreads * U;
-  const int64_t seg = (kTmaCW + g.w + 1) & ~int64_t(1);
+  const int64_t seg = (kTmaCW + m.wmax + 1) & ~int64_t(1);
   const char* env_b = getenv("SSB_EVAL_BATCH");
   const int batch = env_b ? atoi(env_b) : 4;
   const char* env_ns = getenv("SSB_EVAL_STAGES");
@@ -353,25 +421,26 @@ cudaError_t launch_tma_u(const void* sat, const void* sat_sq, EvalGeom g, WinOut
   if (NS < 2) NS = 2;
   if (NS > kTmaMaxNS) NS = kTmaMaxNS;
   const size_t smem = 256 + (size_t)NS * NT * 2 * seg * sizeof(Acc);
-  if (smem > 200 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) || (SQ && (reinterpret_cast<uintptr_t>(sat_sq) & 15)) ||
-      (g.sat_ld & 1))
+  if (smem > 200 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) ||
+      (SQ && (reinterpret_cast<uintptr_t>(sat_sq) & 15)) || (m.sat_ld & 1))
     return cudaSuccess;
   const char* env_mb = getenv("SSB_EVAL_L2_MB");
-  const char* env_k = getenv("SSB_EVAL_ROWS_IN_FLIGHT");
-  const char* env_h = getenv("SSB_EVAL_HINTS");
-  g.hints = env_h ? atoi(env_h) : 0;
-  g.pw = panel_width(g.out_c, g.w, 1, SQ, kTmaCW, (env_mb ? atof(env_mb) : 8.0) * 1024 * 1024);
-  g.n_panels = (g.out_c + g.pw - 1) / g.pw;
-  g.cpp = g.pw / kTmaCW;
-  g.cpl = (g.out_c - (g.n_panels - 1) * g.pw + kTmaCW - 1) / kTmaCW;
-  auto kfn = window_eval_tma_kernel<Acc, SQ, U>;
+  int64_t out_c_max = 0;
+  for (int k = 0; k < m.nwin; ++k) out_c_max = m.out_c[k] > out_c_max ? m.out_c[k] : out_c_max;
+  // multi-window keeps wmax rows of every window's panel hot; scale the budget
+  const double mb = env_mb ? atof(env_mb) : 8.0;
+  m.pw = panel_width_max(out_c_max, m.wmax, SQ, kTmaCW, mb * 1024 * 1024);
+  m.n_panels = (out_c_max + m.pw - 1) / m.pw;
+  m.cpp = m.pw / kTmaCW;
+  m.cpl = (out_c_max - (m.n_panels - 1) * m.pw + kTmaCW - 1) / kTmaCW;
+  const bool multi = m.nwin > 1;
+  auto kfn = multi ? window_eval_tma_kernel<Acc, SQ, U, true> : window_eval_tma_kernel<Acc, SQ, U, false>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads, smem);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-  int blocks = kNumSMs * per_sm;
-  if (env_k && atoi(env_k) > 0 && atoi(env_k) < blocks) blocks = atoi(env_k);
+  const int blocks = kNumSMs * per_sm;
   // one ticket counter per launch, from a small ring (concurrent launches on
   // different streams get different slots)
   static std::atomic<unsigned> slot{0};
@@ -381,10 +450,40 @@ cudaError_t launch_tma_u(const void* sat, const void* sat_sq, EvalGeom g, WinOut
   unsigned long long* ticket = tickets + (slot.fetch_add(1) % 256);
   e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  kfn<<<blocks, kThreads, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq), g, o,
-                                      fin, seg, ticket, NS, batch);
+  kfn<<<blocks, kThreads, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq), m,
+                                      seg, ticket, NS, batch);
   used = true;
   return cudaGetLastError();
+}
+
+template <typename Acc, bool SQ>
+cudaError_t launch_tma_multi(const void* sat, const void* sat_sq, const MultiEval& m, cudaStream_t st, bool& used) {
+  return launch_tma_multi_u<Acc, SQ, 4>(sat, sat_sq, m, st, used);
+}
+
+inline void fill_fin(MultiEval& m, int k, int in_dtype) {
+  const uint64_t w = (uint64_t)m.w[k];
+  m.n[k] = w * w;
+  m.dn[k] = (double)(w * w);
+  const uint64_t maxv = in_dtype == IN_U8 ? 255u : in_dtype == IN_U16 ? 65535u : 2147483648u;
+  // stats.py:28-32: w^4 * max^2 <= 2^64 - 1  <=>  w^2 * max <= 2^32 - 1
+  m.u64_ok[k] = ((unsigned __int128)(w * w) * maxv) <= (unsigned __int128)0xFFFFFFFFull ? 1 : 0;
+}
+
+// single-window wrapper over the multi-window TMA kernel
+template <typename Acc, bool SQ>
+cudaError_t launch_tma(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, int in_dtype, cudaStream_t st,
+                       bool& used) {
+  MultiEval m{};
+  m.nwin = 1;
+  m.mask = g.mask;
+  m.is_signed = in_dtype == IN_I32;
+  m.wmin = m.wmax = g.w;
+  m.R = g.out_r + g.w - 1;
+  m.sat_ld = g.sat_ld;
+  m.w[0] = g.w; m.out_r[0] = g.out_r; m.out_c[0] = g.out_c; m.o[0] = o;
+  fill_fin(m, 0, in_dtype);
+  return launch_tma_multi<Acc, SQ>(sat, sat_sq, m, st, used);
 }
 
 inline EvalGeom make_eval_geom(int64_t R, int64_t C, int64_t w, int64_t s, int64_t sat_ld, int mask, bool sq) {
@@ -407,16 +506,6 @@ inline EvalGeom make_eval_geom(int64_t R, int64_t C, int64_t w, int64_t s, int64
   g.cpl = (last_w + kChunk - 1) / kChunk;
   g.n_items = g.out_r * (g.cpp * (g.n_panels - 1) + g.cpl);
   return g;
-}
-
-template <typename Acc, bool SQ>
-cudaError_t launch_tma(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, cudaStream_t st,
-                       bool& used) {
-  const char* env_u = getenv("SSB_EVAL_UNROLL");
-  const int u = env_u ? atoi(env_u) : 4;
-  if (u == 8) return launch_tma_u<Acc, SQ, 8>(sat, sat_sq, g, o, fin, st, used);
-  if (u == 2) return launch_tma_u<Acc, SQ, 2>(sat, sat_sq, g, o, fin, st, used);
-  return launch_tma_u<Acc, SQ, 4>(sat, sat_sq, g, o, fin, st, used);
 }
 
 template <typename Acc, bool SQ>
@@ -447,13 +536,14 @@ cudaError_t launch_rows(const void* sat, const void* sat_sq, EvalGeom g, WinOut 
 }
 
 template <typename Acc>
-cudaError_t launch_eval_t(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, bool sq, cudaStream_t st) {
+cudaError_t launch_eval_t(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, bool sq, int in_dtype,
+                          cudaStream_t st) {
   if (g.s == 1) {
     const char* env_path = getenv("SSB_EVAL_PATH");  // tuning: "ldg" forces the load-based sweep
     if (!(env_path && env_path[0] == 'l')) {
       bool used = false;
-      cudaError_t e = sq ? launch_tma<Acc, true>(sat, sat_sq, g, o, fin, st, used)
-                         : launch_tma<Acc, false>(sat, sat_sq, g, o, fin, st, used);
+      cudaError_t e = sq ? launch_tma<Acc, true>(sat, sat_sq, g, o, in_dtype, st, used)
+                         : launch_tma<Acc, false>(sat, sat_sq, g, o, in_dtype, st, used);
       if (e != cudaSuccess || used) return e;
     }
     return sq ? launch_rows<Acc, true>(sat, sat_sq, g, o, fin, st) : launch_rows<Acc, false>(sat, sat_sq, g, o, fin, st);
@@ -475,7 +565,7 @@ cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_floa
   cudaError_t e;
   if (is_float) {
     Fin<double> fin{(double)(w * w)};
-    e = launch_eval_t<double>(sat, sat_sq, g, o, fin, sq, st);
+    e = launch_eval_t<double>(sat, sat_sq, g, o, fin, sq, in_dtype, st);
   } else {
     Fin<uint64_t> fin{};
     fin.f.n = (uint64_t)(w * w);
@@ -484,10 +574,44 @@ cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_floa
     // stats.py:28-32: w^4 * max^2 <= 2^64 - 1  <=>  w^2 * max <= 2^32 - 1
     fin.f.u64_ok = ((unsigned __int128)(uint64_t)(w * w) * maxv) <= (unsigned __int128)0xFFFFFFFFull;
     fin.f.is_signed = (in_dtype == IN_I32);
-    e = launch_eval_t<uint64_t>(sat, sat_sq, g, o, fin, sq, st);
+    e = launch_eval_t<uint64_t>(sat, sat_sq, g, o, fin, sq, in_dtype, st);
   }
   note_launch(1);
   return e;
+}
+
+// Several stride-1 windows from one table pass (single kernel); returns
+// cudaErrorNotSupported if the TMA path cannot take this request.
+cudaError_t launch_window_eval_multi(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R,
+                                     int64_t C, int64_t sat_ld, int nwin, const int64_t* ws, int mask, const WinOut* outs,
+                                     cudaStream_t st) {
+  if (nwin < 1 || nwin > kMaxWin) return cudaErrorNotSupported;
+  MultiEval m{};
+  m.nwin = nwin;
+  m.mask = mask;
+  m.is_signed = in_dtype == IN_I32;
+  m.R = R;
+  m.sat_ld = sat_ld;
+  m.wmin = ws[0];
+  m.wmax = ws[0];
+  for (int k = 0; k < nwin; ++k) {
+    m.w[k] = ws[k];
+    m.out_r[k] = R - ws[k] + 1;
+    m.out_c[k] = C - ws[k] + 1;
+    m.o[k] = outs[k];
+    m.wmin = ws[k] < m.wmin ? ws[k] : m.wmin;
+    m.wmax = ws[k] > m.wmax ? ws[k] : m.wmax;
+    fill_fin(m, k, in_dtype);
+  }
+  const bool sq = (mask & ST_STD) != 0;
+  bool used = false;
+  cudaError_t e;
+  if (is_float) e = sq ? launch_tma_multi<double, true>(sat, sat_sq, m, st, used) : launch_tma_multi<double, false>(sat, sat_sq, m, st, used);
+  else e = sq ? launch_tma_multi<uint64_t, true>(sat, sat_sq, m, st, used) : launch_tma_multi<uint64_t, false>(sat, sat_sq, m, st, used);
+  if (e != cudaSuccess) return e;
+  if (!used) return cudaErrorNotSupported;
+  note_launch(1);
+  return cudaSuccess;
 }
 
 }  // namespace ssb

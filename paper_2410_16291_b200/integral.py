@@ -166,16 +166,39 @@ def _finish(img: ImageGrid, stats, res) -> dict:
     return out
 
 
-def _run_tables(img: ImageGrid, wins, stat: StatKind, sum_sat=None, sq_sat=None):
-    """Tables once, then one corner sweep per window (integral.py:166-189, :199-210)."""
+def _run_tables(img: ImageGrid, wins, stat: StatKind):
+    """Tables once, then the corner sweep(s) (integral.py:166-189, :199-210).
+
+    Stride-1 window sets go through ssb_window_eval_multi: one pass over the
+    table serves every window."""
+    import ctypes
+
     x, dev = _engine.device_input(img)
     flag = _engine.new_flag(dev) if img.elem_kind is ElemKind.F32 else None
     sq_needed = needs_squares(stat)
     sat, sq, ld = _engine.build_tables(x, img.elem_kind, img.rows, img.cols, dev, squared=sq_needed, flag=flag)
     results = []
-    for win in wins:
-        res = _engine.eval_tables(sat, sq, ld, img.elem_kind, img.rows, img.cols, win.w, win.stride, (stat,), dev)
-        results.append(res)
+    if len(wins) > 1 and all(w.stride == 1 for w in wins):
+        lib = _lib.load()
+        outs = [_engine.alloc_outputs(img.elem_kind, (stat,), img.rows - w.w + 1, img.cols - w.w + 1, dev)[stat]
+                for w in wins]
+        n = len(wins)
+        arr = lambda t, vals: (t * n)(*vals)  # noqa: E731
+        ptrs = [int(o.data_ptr()) for o in outs]
+        none = [None] * n
+        rc = lib.ssb_window_eval_multi(
+            int(sat.data_ptr()), None if sq is None else int(sq.data_ptr()), img.elem_kind.abi_code, img.rows,
+            img.cols, ld, n, arr(ctypes.c_int64, [w.w for w in wins]), stat.bit,
+            arr(ctypes.c_void_p, ptrs if stat is StatKind.SUM else none),
+            arr(ctypes.c_void_p, ptrs if stat is StatKind.MEAN else none),
+            arr(ctypes.c_void_p, ptrs if stat is StatKind.STD else none),
+            arr(ctypes.c_int64, [img.cols - w.w + 1 for w in wins]), _device.stream_ptr(dev))
+        _lib.check(rc, "multi-window evaluation")
+        results = [{stat: o} for o in outs]
+    else:
+        for win in wins:
+            results.append(_engine.eval_tables(sat, sq, ld, img.elem_kind, img.rows, img.cols, win.w, win.stride,
+                                               (stat,), dev))
     _engine.check_nonfinite(flag)
     return [ResultGrid(stat, _finish(img, (stat,), r)[stat]) for r in results]
 
