@@ -259,7 +259,7 @@ template <> struct FinK<double> {
 };
 
 template <typename Acc, bool SQ, int U, bool MULTI>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads + 32)
 window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, const __grid_constant__ MultiEval g,
                        int64_t seg, unsigned long long* __restrict__ ticket, int NS, int batch) {
   constexpr int NT = SQ ? 2 : 1;
@@ -306,53 +306,50 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
     i = (int64_t)rb_off + g.wmin - g.w[k];
     return i >= 0 && i < g.out_r[k] && j0 < g.out_c[k];
   };
-  bool producing = true;
-  // tickets come in batches of `batch` consecutive items (one atomic per
-  // batch); the next batch is requested while the current one is issued
-  int64_t cur = 0, cur_end = 0, next_b = 0;
-  if (tid == 0) next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
-  auto produce = [&](int64_t m) {  // thread 0 only
-    const int s = (int)(m % NS);
-    if (m >= NS) mbar_wait(&empty[s], (uint32_t)(((m / NS) - 1) & 1));
-    if (cur == cur_end) {
-      cur = next_b;
-      cur_end = next_b + batch;
-      if (cur < total) next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+  // warp 8 is the producer (one elected lane); warps 0-7 consume
+  if (tid >= kThreads) {
+    if (lane != 0) return;
+    int64_t cur = 0, cur_end = 0;
+    int64_t next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+    for (int64_t m = 0;; ++m) {
+      const int s = (int)(m % NS);
+      if (m >= NS) mbar_wait(&empty[s], (uint32_t)(((m / NS) - 1) & 1));
+      if (cur == cur_end) {  // tickets come in batches; the next batch is requested ahead
+        cur = next_b;
+        cur_end = next_b + batch;
+        if (cur < total) next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+      }
+      const int64_t it = cur++;
+      if (it >= total) {
+        meta[s] = -1;
+        mbar_arrive_expect_tx(&full[s], 0);
+        return;
+      }
+      int64_t i, j0;
+      int k;
+      if (!coords(it, i, k, j0)) {
+        meta[s] = -2;
+        mbar_arrive_expect_tx(&full[s], 0);
+        continue;
+      }
+      meta[s] = it;
+      const int64_t w = g.w[k];
+      const int64_t need = (kTmaCW + w + 1) & ~int64_t(1);
+      int64_t len = ld - j0 < need ? ld - j0 : need;
+      len &= ~int64_t(1);
+      const uint32_t bytes = (uint32_t)(len * 8);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full[s], bytes * 2 * NT);
+      Acc* b = buf + (int64_t)s * NT * 2 * seg;
+      bulk_g2s(b, sat + i * ld + j0, bytes, &full[s]);
+      bulk_g2s(b + seg, sat + (i + w) * ld + j0, bytes, &full[s]);
+      if constexpr (SQ) {
+        bulk_g2s(b + 2 * seg, sq + i * ld + j0, bytes, &full[s]);
+        bulk_g2s(b + 3 * seg, sq + (i + w) * ld + j0, bytes, &full[s]);
+      }
     }
-    const int64_t it = cur++;
-    if (it >= total) {
-      meta[s] = -1;
-      producing = false;
-      mbar_arrive_expect_tx(&full[s], 0);
-      return;
-    }
-    int64_t i, j0;
-    int k;
-    if (!coords(it, i, k, j0)) {
-      meta[s] = -2;
-      mbar_arrive_expect_tx(&full[s], 0);
-      return;
-    }
-    meta[s] = it;
-    const int64_t w = g.w[k];
-    const int64_t need = (kTmaCW + w + 1) & ~int64_t(1);
-    int64_t len = ld - j0 < need ? ld - j0 : need;
-    len &= ~int64_t(1);
-    const uint32_t bytes = (uint32_t)(len * 8);
-    fence_proxy_async();
-    mbar_arrive_expect_tx(&full[s], bytes * 2 * NT);
-    Acc* b = buf + (int64_t)s * NT * 2 * seg;
-    bulk_g2s(b, sat + i * ld + j0, bytes, &full[s]);
-    bulk_g2s(b + seg, sat + (i + w) * ld + j0, bytes, &full[s]);
-    if constexpr (SQ) {
-      bulk_g2s(b + 2 * seg, sq + i * ld + j0, bytes, &full[s]);
-      bulk_g2s(b + 3 * seg, sq + (i + w) * ld + j0, bytes, &full[s]);
-    }
-  };
-  if (tid == 0)
-    for (int64_t m = 0; m < NS - 1 && producing; ++m) produce(m);
+  }
   for (int64_t m = 0;; ++m) {
-    if (tid == 0 && producing) produce(m + NS - 1);
     const int s = (int)(m % NS);
     mbar_wait(&full[s], (uint32_t)((m / NS) & 1));
     const int64_t it = meta[s];
@@ -417,7 +414,7 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   const char* env_b = getenv("SSB_EVAL_BATCH");
   const int batch = env_b ? atoi(env_b) : 4;
   const char* env_ns = getenv("SSB_EVAL_STAGES");
-  int NS = env_ns ? atoi(env_ns) : 2;
+  int NS = env_ns ? atoi(env_ns) : 3;
   if (NS < 2) NS = 2;
   if (NS > kTmaMaxNS) NS = kTmaMaxNS;
   const size_t smem = 256 + (size_t)NS * NT * 2 * seg * sizeof(Acc);
@@ -438,7 +435,7 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads + 32, smem);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   const int blocks = kNumSMs * per_sm;
   // one ticket counter per launch, from a small ring (concurrent launches on
@@ -450,8 +447,8 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   unsigned long long* ticket = tickets + (slot.fetch_add(1) % 256);
   e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  kfn<<<blocks, kThreads, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq), m,
-                                      seg, ticket, NS, batch);
+  kfn<<<blocks, kThreads + 32, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq),
+                                           m, seg, ticket, NS, batch);
   used = true;
   return cudaGetLastError();
 }
