@@ -7,6 +7,7 @@ torch stream; nothing computes on the host.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -55,21 +56,63 @@ def new_flag(device):
     return t.zeros(1, dtype=t.int32, device=device)
 
 
+class _Scratch(threading.local):
+    """Grow-only per-thread, per-device scratch buffers for tables that never
+    leave the library (swa / multi_window), so repeated calls do not churn
+    multi-GB allocations through the caching allocator.  Thread-local, so
+    concurrent callers never share a buffer.  release_scratch() frees them."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key, nbytes: int, device):
+        cur = self.bufs.get((key, str(device)))
+        if cur is None or cur.numel() < nbytes:
+            self.bufs.pop((key, str(device)), None)
+            cur = _device.empty((max(nbytes, 8),), np.uint8, device, f"{nbytes} bytes of scratch")
+            self.bufs[(key, str(device))] = cur
+        return cur
+
+    def clear(self):
+        self.bufs.clear()
+
+
+_SCRATCH = _Scratch()
+
+
+def release_scratch() -> None:
+    """Free the cached scratch tables (they are reused across swa/multi_window calls)."""
+    _SCRATCH.clear()
+    t = _device.torch()
+    if t.cuda.is_available():
+        t.cuda.empty_cache()
+
+
+def _table_view(buf, rows: int, ld: int, acc_dt):
+    n = (rows + 1) * ld
+    return buf[: n * 8].view(_device.storage_dtype(acc_dt)).view(rows + 1, ld)
+
+
 def build_tables(x, kind: ElemKind, rows: int, cols: int, device, *, squared: bool, plain: bool = True,
-                 carry=None, carry_sq=None, flag=None):
+                 carry=None, carry_sq=None, flag=None, scratch: bool = False):
     """Build the (rows+1) x (cols+1) table(s) in HBM.  Returns (sat, sat_sq, sat_ld).
 
-    ``plain=False`` with ``squared=True`` builds only the squared table (build_sat(img, squared=True))."""
+    ``plain=False`` with ``squared=True`` builds only the squared table (build_sat(img, squared=True)).
+    ``scratch=True`` places the tables in the reusable scratch cache (callers that do not return them)."""
     lib = _lib.load()
     ld = sat_ld_for(cols)
     acc_dt = np.float64 if kind is ElemKind.F32 else np.uint64
+    tbytes = (rows + 1) * ld * 8
+    what = f"a {rows + 1}x{cols + 1} integral table"
     sat = sq = None
     if plain:
-        sat = _device.empty((rows + 1, ld), acc_dt, device, f"a {rows + 1}x{cols + 1} integral table")
+        sat = (_table_view(_SCRATCH.get("sat", tbytes, device), rows, ld, acc_dt) if scratch
+               else _device.empty((rows + 1, ld), acc_dt, device, what))
     if squared:
-        sq = _device.empty((rows + 1, ld), acc_dt, device, f"a {rows + 1}x{cols + 1} integral table")
+        sq = (_table_view(_SCRATCH.get("sat_sq", tbytes, device), rows, ld, acc_dt) if scratch
+              else _device.empty((rows + 1, ld), acc_dt, device, what))
     ws_bytes = int(lib.ssb_sat_workspace_bytes(kind.abi_code, rows, cols, 1 if squared else 0))
-    ws = _device.empty((max(ws_bytes, 8),), np.uint8, device, "table workspace")
+    ws = _SCRATCH.get("ws", ws_bytes, device)
     st = _device.stream_ptr(device)
     rc = lib.ssb_sat_build(_ptr(x), kind.abi_code, rows, cols, cols, _ptr(sat), _ptr(sq), ld, _ptr(carry),
                            _ptr(carry_sq), _ptr(ws), ws_bytes, _ptr(flag), st)
@@ -123,7 +166,7 @@ def choose_pipeline(pipeline: str, kind: ElemKind, w: int, stride: int) -> str:
     # auto: integer results are exact on both pipelines, so take the cheaper
     # one; float results keep the table pipeline so swa/multi_window/swa_integral
     # agree bit for bit (integral.py:199-204).
-    return "fused" if (fusable and kind.is_integer) else "table"
+    return "fused" if (fusable and kind in (ElemKind.U8, ElemKind.U16)) else "table"
 
 
 def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None):
@@ -136,7 +179,7 @@ def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto
         res = fused(x, img.elem_kind, rows, cols, w, stats, dev, flag=flag, outs=outs)
     else:
         need_sq = StatKind.STD in stats
-        sat, sq, ld = build_tables(x, img.elem_kind, rows, cols, dev, squared=need_sq, flag=flag)
+        sat, sq, ld = build_tables(x, img.elem_kind, rows, cols, dev, squared=need_sq, flag=flag, scratch=True)
         res = eval_tables(sat, sq, ld, img.elem_kind, rows, cols, w, stride, stats, dev, outs=outs)
     check_nonfinite(flag)
     return res

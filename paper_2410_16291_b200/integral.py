@@ -176,7 +176,8 @@ def _run_tables(img: ImageGrid, wins, stat: StatKind):
     x, dev = _engine.device_input(img)
     flag = _engine.new_flag(dev) if img.elem_kind is ElemKind.F32 else None
     sq_needed = needs_squares(stat)
-    sat, sq, ld = _engine.build_tables(x, img.elem_kind, img.rows, img.cols, dev, squared=sq_needed, flag=flag)
+    sat, sq, ld = _engine.build_tables(x, img.elem_kind, img.rows, img.cols, dev, squared=sq_needed, flag=flag,
+                                       scratch=True)
     results = []
     if len(wins) > 1 and all(w.stride == 1 for w in wins):
         lib = _lib.load()
