@@ -20,6 +20,8 @@
  *                        copies, compute, device->host copies, streamed by bands
  *
  * Conventions
+ *   - Device rasters must be 16-byte aligned (rows are staged with TMA bulk
+ *     copies); tables 16-byte aligned with an even pitch.
  *   - Every device pointer is caller-allocated device memory; the library keeps
  *     no persistent allocations (ssb_swa_host allocates and frees its own
  *     staging per call).

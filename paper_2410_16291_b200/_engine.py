@@ -35,9 +35,15 @@ def sat_ld_for(cols: int) -> int:
 
 
 def device_input(img: ImageGrid):
-    """Return (device tensor, device) for an ImageGrid, copying host rasters once."""
+    """Return (device tensor, device) for an ImageGrid, copying host rasters once.
+
+    Device rasters must be 16-byte aligned for the TMA row staging; an unaligned
+    view (e.g. a row slice) is copied once."""
     if img.on_device:
-        return img.values, img.values.device
+        x = img.values
+        if x.data_ptr() % 16:
+            x = x.clone()
+        return x, x.device
     dev = _device.current_device()
     return _device.to_device(img.values, dev), dev
 

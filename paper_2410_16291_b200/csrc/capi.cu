@@ -69,6 +69,11 @@ int check_image(int dtype, int64_t rows, int64_t cols, int64_t in_ld) {
   return SSB_OK;
 }
 
+int check_aligned(const void* p, const char* what) {
+  if (reinterpret_cast<uintptr_t>(p) & 15) return fail(SSB_EINVAL, "%s must be 16-byte aligned", what);
+  return SSB_OK;
+}
+
 int check_window(int64_t rows, int64_t cols, int64_t w, int64_t stride) {
   if (w < 1) return fail(SSB_EINVAL, "window size must be >= 1, got %lld", (long long)w);
   if (stride < 1) return fail(SSB_EINVAL, "stride must be >= 1, got %lld", (long long)stride);
@@ -112,6 +117,7 @@ int ssb_sat_prepare(const void* in, int in_dtype, int64_t rows, int64_t cols, in
   int rc = check_image(in_dtype, rows, cols, in_ld);
   if (rc) return rc;
   if (in_dtype == SSB_I32 && with_squares) return fail(SSB_EUNSUPPORTED, "squared tables are not supported for int32 input");
+  if ((rc = check_aligned(in, "input raster"))) return rc;
   const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, with_squares != 0);
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
   cudaError_t e = launch_sat_prepare(in_dtype, in, rows, cols, in_ld, with_squares != 0, ws, band_totals,
@@ -124,6 +130,7 @@ int ssb_sat_finish(const void* in, int in_dtype, int64_t rows, int64_t cols, int
   int rc = check_image(in_dtype, rows, cols, in_ld);
   if (rc) return rc;
   if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
+  if ((rc = check_aligned(in, "input raster"))) return rc;
   if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
   if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
     return fail(SSB_EINVAL, "tables must be 16-byte aligned");
@@ -217,6 +224,7 @@ int ssb_window_fused(const void* in, int in_dtype, int64_t rows, int64_t cols, i
   if ((rc = check_window(rows, cols, w, 1))) return rc;
   if ((rc = check_stats(in_dtype, stat_mask))) return rc;
   if (w > kFusedMaxWindow) return fail(SSB_EUNSUPPORTED, "fused path supports w <= %lld", (long long)kFusedMaxWindow);
+  if ((rc = check_aligned(in, "input raster"))) return rc;
   if (((stat_mask & SSB_SUM) && !out_sum) || ((stat_mask & SSB_MEAN) && !out_mean) || ((stat_mask & SSB_STD) && !out_std))
     return fail(SSB_EINVAL, "missing output buffer");
   if (out_ld < cols - w + 1) return fail(SSB_EINVAL, "out_ld < output cols");

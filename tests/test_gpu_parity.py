@@ -300,3 +300,63 @@ def test_reference_seams(sb, rng):
                 np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-9)
             else:
                 np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("shape,w,stride", [((1, 1), 1, 1), ((1, 4097), 1, 1), ((4097, 1), 1, 3), ((3, 70001), 3, 1),
+                                            ((5000, 7), 7, 1), ((33, 33), 33, 1), ((257, 300), 256, 1),
+                                            ((700, 701), 5, 9), ((4000, 3300), 3200, 1), ((300, 300), 17, 17)])
+def test_edge_shapes(sb, shape, w, stride):
+    """Degenerate and ragged shapes: 1-pixel images, single rows/columns, w = min dim,
+    stride > w, windows wider than the fused path (table fallback)."""
+    rng = np.random.default_rng(sum(shape) + w)
+    for kind in ("u8", "u16", "f32"):
+        v = random_values(rng, *shape, kind)
+        for stat in ("sum", "std"):
+            got = sb.swa(v, w, stat, stride=stride)
+            assert_matches(got, O.swa(v, w, stat, stride), v, stat, w)
+
+
+def test_unaligned_device_view(sb):
+    """A row-slice view whose data pointer is not 16-byte aligned is handled (copied once)."""
+    rng = np.random.default_rng(3)
+    v = random_values(rng, 41, 37, "u8")
+    d = to_dev(v)
+    view = d[1:]  # offset 37 bytes
+    assert view.data_ptr() % 16 != 0
+    for pipe in PIPES:
+        got = host(sb.swa(view, 5, "sum", pipeline=pipe), np.uint64)
+        np.testing.assert_array_equal(got, O.swa(v[1:], 5, "sum"))
+
+
+def test_capi_rejects_unaligned_raster(sb):
+    from paper_2410_16291_b200 import _lib
+
+    lib = _lib.load()
+    d = to_dev(np.zeros((8, 40), np.uint8))
+    rc = lib.ssb_window_fused(d.data_ptr() + 1, _lib.U8, 4, 40, 40, 3, _lib.SUM, d.data_ptr(), None, None, 38, None, 0,
+                              None)
+    assert rc == _lib.EINVAL and b"aligned" in lib.ssb_last_error()
+
+
+def test_concurrent_threads(sb):
+    """The facade is reentrant: concurrent callers get correct, independent results."""
+    import threading
+
+    rng = np.random.default_rng(8)
+    imgs = [random_values(rng, 300 + 7 * k, 290, "u16") for k in range(6)]
+    refs = [O.swa(v, 11, "mean") for v in imgs]
+    errs = []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                np.testing.assert_array_equal(sb.swa(imgs[k], 11, "mean", pipeline="table"), refs[k])
+        except Exception as exc:  # pragma: no cover
+            errs.append(exc)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
