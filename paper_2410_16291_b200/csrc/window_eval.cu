@@ -267,8 +267,11 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + kTmaMaxNS;
-  int64_t* meta = reinterpret_cast<int64_t*>(empty + kTmaMaxNS);  // [NS] item of each stage (-1 done, -2 skip)
-  Acc* buf = reinterpret_cast<Acc*>(smem_raw + 256);              // [NS][NT][2][seg]
+  // per stage: decoded item (output row i, -1 done, -2 skip), first column j0, window k
+  int64_t* meta = reinterpret_cast<int64_t*>(empty + kTmaMaxNS);
+  int64_t* meta_j0 = meta + kTmaMaxNS;
+  int* meta_k = reinterpret_cast<int*>(meta_j0 + kTmaMaxNS);
+  Acc* buf = reinterpret_cast<Acc*>(smem_raw + 384);              // [NS][NT][2][seg]
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ld = g.sat_ld;
   const int64_t nrb = g.R + 1 - g.wmin;  // bottom rows wmin..R
@@ -332,7 +335,9 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
         mbar_arrive_expect_tx(&full[s], 0);
         continue;
       }
-      meta[s] = it;
+      meta[s] = i;
+      meta_j0[s] = j0;
+      meta_k[s] = k;
       const int64_t w = g.w[k];
       const int64_t need = (kTmaCW + w + 1) & ~int64_t(1);
       int64_t len = ld - j0 < need ? ld - j0 : need;
@@ -352,16 +357,15 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
   for (int64_t m = 0;; ++m) {
     const int s = (int)(m % NS);
     mbar_wait(&full[s], (uint32_t)((m / NS) & 1));
-    const int64_t it = meta[s];
-    if (it == -1) break;
-    if (it == -2) {
+    const int64_t i = meta[s];
+    if (i == -1) break;
+    if (i == -2) {
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
       continue;
     }
-    int64_t i, j0;
-    int k;
-    coords(it, i, k, j0);
+    const int64_t j0 = meta_j0[s];
+    const int k = meta_k[s];
     const int64_t w = g.w[k];
     const Acc* T = buf + (int64_t)s * NT * 2 * seg;
     const Acc* B = T + seg;
@@ -417,7 +421,7 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   int NS = env_ns ? atoi(env_ns) : 3;
   if (NS < 2) NS = 2;
   if (NS > kTmaMaxNS) NS = kTmaMaxNS;
-  const size_t smem = 256 + (size_t)NS * NT * 2 * seg * sizeof(Acc);
+  const size_t smem = 384 + (size_t)NS * NT * 2 * seg * sizeof(Acc);
   if (smem > 200 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) ||
       (SQ && (reinterpret_cast<uintptr_t>(sat_sq) & 15)) || (m.sat_ld & 1))
     return cudaSuccess;

@@ -62,7 +62,8 @@ def main():
             bytes_ = nin + (2 * T * n_tab if pipe == "table" else 0) + outs
             print(json.dumps({"config": name, "pipeline": pipe, "ms": round(ms, 3),
                               "gpx_s": round(R * C / ms / 1e6, 1), "alg_GB": round(bytes_ / 1e9, 2),
-                              "roofline_frac": round(bytes_ / ms / 1e6 / PEAK, 3), "gen_s": round(gen, 1)}), flush=True)
+                              "roofline_frac": round(bytes_ / ms / 1e6 / PEAK, 3), "gen_s": round(gen, 1),
+                              "alloc_retries": torch.cuda.memory_stats().get("num_alloc_retries", 0)}), flush=True)
             torch.cuda.empty_cache()
         del x
         torch.cuda.empty_cache()
