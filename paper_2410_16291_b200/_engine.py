@@ -170,9 +170,17 @@ def choose_pipeline(pipeline: str, kind: ElemKind, w: int, stride: int) -> str:
     if pipeline == "table":
         return "table"
     # auto: integer results are exact on both pipelines, so take the cheaper
-    # one; float results keep the table pipeline so swa/multi_window/swa_integral
-    # agree bit for bit (integral.py:199-204).
-    return "fused" if (fusable and kind in (ElemKind.U8, ElemKind.U16)) else "table"
+    # one (measured, scripts/pipe_probe.py: the fused strip kernel wins for
+    # uint8 with w <= 256 and uint16 with w <= 128); float results keep the
+    # table pipeline so swa/multi_window/swa_integral agree bit for bit
+    # (integral.py:199-204).
+    if not fusable:
+        return "table"
+    if kind is ElemKind.U8 and w <= 256:
+        return "fused"
+    if kind is ElemKind.U16 and w <= 128:
+        return "fused"
+    return "table"
 
 
 def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None):
