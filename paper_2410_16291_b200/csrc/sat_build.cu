@@ -33,6 +33,10 @@
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
 
+#ifndef SSB_SCAN_MINB
+#define SSB_SCAN_MINB 2
+#endif
+
 namespace ssb {
 
 // ---- tile geometry -----------------------------------------------------------
@@ -466,7 +470,7 @@ __device__ __forceinline__ void store_lane_cols(Acc* __restrict__ dst, const Acc
 }
 
 template <typename InT, bool SQ>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SQ ? 2 : SSB_SCAN_MINB)
 sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                 typename Elem<InT>::Acc* __restrict__ sat, typename Elem<InT>::Acc* __restrict__ sat_sq, int64_t sat_ld,
                 const typename Elem<InT>::Acc* __restrict__ rl, const typename Elem<InT>::Acc* __restrict__ rl_sq,
