@@ -28,6 +28,7 @@
 // where RPloc is the strip-local row prefix.  Integer tables are exact modulo
 // 2^64; f32 input accumulates in double with a deterministic order.
 #include <climits>
+#include <cstdlib>
 
 #include "ssb_async.cuh"
 #include "ssb_common.cuh"
@@ -138,24 +139,25 @@ __device__ __forceinline__ bool any_nonfinite(const uint32_t* o) {
 // transpose and no CTA-wide barrier anywhere in the sweep.
 constexpr int kWarpsPerCta = kThreads / 32;
 
-template <typename InT>
+template <typename InT, int RB_ = 0>
 struct WarpStage {
   using G = Geo<InT>;
-  static constexpr int RBW = G::ES == 1 ? 8 : 4;  // rows per stage (<= 32)
+  static constexpr int RBW = RB_ > 0 ? RB_ : (G::ES == 1 ? 8 : 4);  // rows per stage (<= 32)
   alignas(16) unsigned char buf[2][RBW * G::ROWB];
   int offs[2][RBW];
   uint64_t bar[2];
 };
 
+template <int WPC = kWarpsPerCta>
 __device__ __forceinline__ void warp_tile(int nJ, int nK, int& J, int& K) {
-  const int t = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const int t = blockIdx.x * WPC + (threadIdx.x >> 5);
   J = t % nJ;
   K = t / nJ;
   if (K >= nK) K = -1;
 }
 
-template <typename InT>
-__device__ __forceinline__ void warp_stage_init(WarpStage<InT>& ws, int lane) {
+template <typename WS>
+__device__ __forceinline__ void warp_stage_init(WS& ws, int lane) {
   if (lane == 0) {
     mbar_init(&ws.bar[0], 1);
     mbar_init(&ws.bar[1], 1);
@@ -210,8 +212,8 @@ __device__ __forceinline__ T warp_reduce_scatter(T (&v)[N], int lane) {
 
 // ---------------------------------------------------------------------------
 // phase 1
-template <typename InT, bool SQ>
-__global__ void __launch_bounds__(kThreads)
+template <typename InT, bool SQ, int RBR, int WPC>
+__global__ void __launch_bounds__(32 * WPC)
 sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                   typename Elem<InT>::Acc* __restrict__ rowtot, typename Elem<InT>::Acc* __restrict__ rowtot_sq,
                   typename Elem<InT>::Acc* __restrict__ colp, typename Elem<InT>::Acc* __restrict__ colp_sq,
@@ -221,14 +223,14 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
   using LocSq = typename Tr::LocSq;
   using Acc = typename Tr::Acc;
   using G = Geo<InT>;
-  using WS = WarpStage<InT>;
+  using WS = WarpStage<InT, RBR>;
   constexpr int TW = G::TW, E = G::E, RB = WS::RBW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WS* stages = reinterpret_cast<WS*>(smem_raw);
   const int lane = threadIdx.x & 31;
   WS& ws = stages[threadIdx.x >> 5];
   int J, K;
-  warp_tile(nJ, nK, J, K);
+  warp_tile<WPC>(nJ, nK, J, K);
   if (K < 0) return;
   const int64_t PR = R + 1, PC = C + 1;
   const int64_t j0 = (int64_t)J * TW, k0 = (int64_t)K * SR;
@@ -591,6 +593,28 @@ inline SatPlan make_sat_plan(int dtype, int64_t R, int64_t C, bool sq) {
 }
 
 
+template <typename InT, bool SQ, int RBR, int WPC>
+cudaError_t launch_reduce_rw(const InT* x, int64_t R, int64_t C, int64_t in_ld, typename Elem<InT>::Acc* rowtot,
+                             typename Elem<InT>::Acc* rowtot_sq, typename Elem<InT>::Acc* colp,
+                             typename Elem<InT>::Acc* colp_sq, int* nonfinite, cudaStream_t st, const SatPlan& p) {
+  const int tb = (int)(((int64_t)p.nJ * p.nK + WPC - 1) / WPC);
+  const int smem = (int)(sizeof(WarpStage<InT, RBR>) * WPC);
+  auto kfn = sat_reduce_kernel<InT, SQ, RBR, WPC>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kfn<<<tb, 32 * WPC, smem, st>>>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ, p.nK, nonfinite);
+  return cudaGetLastError();
+}
+
+// Reduce kernel shape: 8-row stages, 8 warps per CTA (measured best among
+// 4/8/16/32-row stages x 4/8 warps at C5).
+template <typename InT, bool SQ>
+cudaError_t launch_reduce_cfg(const InT* x, int64_t R, int64_t C, int64_t in_ld, typename Elem<InT>::Acc* rowtot,
+                              typename Elem<InT>::Acc* rowtot_sq, typename Elem<InT>::Acc* colp,
+                              typename Elem<InT>::Acc* colp_sq, int* nonfinite, cudaStream_t st, const SatPlan& p) {
+  return launch_reduce_rw<InT, SQ, 0, kWarpsPerCta>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, nonfinite, st, p);
+}
+
 template <typename InT, bool SQ>
 cudaError_t launch_sat_prepare_t(const void* in, int64_t R, int64_t C, int64_t in_ld, void* ws, void* totals,
                                  void* totals_sq, int* nonfinite, cudaStream_t st, const SatPlan& p) {
@@ -603,12 +627,8 @@ cudaError_t launch_sat_prepare_t(const void* in, int64_t R, int64_t C, int64_t i
   Acc* srl = w + p.off_srl;
   Acc* srl_sq = SQ ? w + p.off_srl_sq : nullptr;
   const InT* x = reinterpret_cast<const InT*>(in);
-  const int tb = (int)(((int64_t)p.nJ * p.nK + kWarpsPerCta - 1) / kWarpsPerCta);
-  const int smem = (int)(sizeof(WarpStage<InT>) * kWarpsPerCta);
-  cudaError_t e = cudaFuncSetAttribute(sat_reduce_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = launch_reduce_cfg<InT, SQ>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, nonfinite, st, p);
   if (e != cudaSuccess) return e;
-  sat_reduce_kernel<InT, SQ><<<tb, kThreads, smem, st>>>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ,
-                                                      p.nK, nonfinite);
   const int nb_rows = (int)((p.PR + kThreads / 32 - 1) / (kThreads / 32));
   sat_rowcarry_kernel<Acc><<<nb_rows, kThreads, 0, st>>>(rowtot, p.nJ, p.PR);
   if (SQ) sat_rowcarry_kernel<Acc><<<nb_rows, kThreads, 0, st>>>(rowtot_sq, p.nJ, p.PR);
