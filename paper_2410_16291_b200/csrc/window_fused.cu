@@ -242,11 +242,11 @@ cudaError_t launch_fused_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
 // sums V of image columns [l E, l E + E) in registers -- for uint8 with
 // w <= 256 two columns per register as 16-bit halves (V <= 65280).  Per
 // finished row the lane-serial prefix + one warp scan give P, written to a
-// per-warp smem buffer with one pad word per lane block (column t at word
-// t + t / E: conflict-free for the lane-contiguous writes because E + 1 is odd,
-// and nearly so for the lane-consecutive reads), so out[j] = P[j+w] - P[j] is
-// read and stored by consecutive lanes (coalesced 8-byte stores).  No CTA
-// barrier anywhere.
+// per-warp smem buffer with one pad word per 32 (P[u] at word u + u / 32:
+// lane-consecutive reads are conflict-free and advance by a constant 33 words
+// per 32 outputs; the lane-contiguous writes see at most 2-way conflicts), so
+// out[j] = P[j+w] - P[j] is read and stored by consecutive lanes (coalesced
+// 8-byte stores).  No CTA barrier anywhere.
 constexpr int kStripWarps = 4;  // warps per CTA
 
 template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ>
@@ -256,8 +256,8 @@ struct StripSmem {
   alignas(16) unsigned char stage[2][2 * RB][ROWB];
   int offs[2][2 * RB];
   uint64_t bar[2];
-  VT p[NV + 32];                  // inclusive prefix of column t at word t + t / E
-  VQ pq[SQ ? NV + 32 : 1];
+  VT p[NV + 64];                  // P[u] = sum of columns < u, at word u + u / 32
+  VQ pq[SQ ? NV + 64 : 1];
 };
 
 template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ, bool PACK>
@@ -314,7 +314,9 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
 #pragma unroll
   for (int k = 0; k < E; ++k) Vq[k] = VQ(0);
   bool nf = false;
-  const int wbase = lane * (E + 1);  // word of this lane's first column
+  const int ubase = lane * E + 1;                        // first P index this lane writes
+  const int addr_a = lane;                               // word of P[lane]
+  const int addr_b = lane + w + ((lane + w) >> 5);       // word of P[lane + w]
 
   for (int b = 0; b < nblk; ++b) {
     const int s = b & 1;
@@ -325,36 +327,59 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
     for (int q = 0; q < RB; ++q) {
       const int64_t r = rb + q;
       if (r >= r_end) break;
-      uint32_t on[NW], oo[NW];
-      lane_elems_packed<InT, E>(sm.stage[s][q], sm.offs[s][q], c0, g.C, on);
-      lane_elems_packed<InT, E>(sm.stage[s][RB + q], sm.offs[s][RB + q], c0, g.C, oo);  // zeros until r >= r_beg + w
-      if constexpr (PACK) {
-        // V[2i] holds columns 4i, 4i+2 and V[2i+1] columns 4i+1, 4i+3 (16-bit halves)
+      {
+        uint32_t oo[NW];  // row r-w (zeros until r >= r_beg + w) leaves the window first
+        lane_elems_packed<InT, E>(sm.stage[s][RB + q], sm.offs[s][RB + q], c0, g.C, oo);
+        if constexpr (PACK) {
+          // V[2i] holds columns 4i, 4i+2 and V[2i+1] columns 4i+1, 4i+3 (16-bit halves;
+          // V >= the leaving row per column, so no borrow crosses a half)
 #pragma unroll
-        for (int i = 0; i < NW; ++i) {
-          V[2 * i] += (on[i] & 0x00FF00FFu);
-          V[2 * i] -= (oo[i] & 0x00FF00FFu);
-          V[2 * i + 1] += ((on[i] >> 8) & 0x00FF00FFu);
-          V[2 * i + 1] -= ((oo[i] >> 8) & 0x00FF00FFu);
+          for (int i = 0; i < NW; ++i) {
+            V[2 * i] -= (oo[i] & 0x00FF00FFu);
+            V[2 * i + 1] -= ((oo[i] >> 8) & 0x00FF00FFu);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k) V[k] = sub(V[k], tv<VT>(elem<InT>(oo, k)));
         }
-      } else {
+        if constexpr (SQ) {
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          const InT xn = elem<InT>(on, k), xo = elem<InT>(oo, k);
-          V[k] = sub(add(V[k], tv<VT>(xn)), tv<VT>(xo));
-          if constexpr (kFloat) nf |= is_nonfinite(xn);
+          for (int k = 0; k < E; ++k) {
+            const InT xo = elem<InT>(oo, k);
+            if constexpr (kFloat) Vq[k] = sub(Vq[k], __dmul_rn((double)xo, (double)xo));
+            else Vq[k] = sub(Vq[k], tv<VQ>(xo) * tv<VQ>(xo));
+          }
         }
       }
-      if constexpr (SQ) {
+      {
+        uint32_t on[NW];
+        lane_elems_packed<InT, E>(sm.stage[s][q], sm.offs[s][q], c0, g.C, on);
+        if constexpr (PACK) {
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          const InT xn = elem<InT>(on, k), xo = elem<InT>(oo, k);
-          if constexpr (kFloat) Vq[k] = sub(add(Vq[k], __dmul_rn((double)xn, (double)xn)), __dmul_rn((double)xo, (double)xo));
-          else Vq[k] = sub(add(Vq[k], tv<VQ>(xn) * tv<VQ>(xn)), tv<VQ>(xo) * tv<VQ>(xo));
+          for (int i = 0; i < NW; ++i) {
+            V[2 * i] += (on[i] & 0x00FF00FFu);
+            V[2 * i + 1] += ((on[i] >> 8) & 0x00FF00FFu);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const InT xn = elem<InT>(on, k);
+            V[k] = add(V[k], tv<VT>(xn));
+            if constexpr (kFloat) nf |= is_nonfinite(xn);
+          }
+        }
+        if constexpr (SQ) {
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const InT xn = elem<InT>(on, k);
+            if constexpr (kFloat) Vq[k] = add(Vq[k], __dmul_rn((double)xn, (double)xn));
+            else Vq[k] = add(Vq[k], tv<VQ>(xn) * tv<VQ>(xn));
+          }
         }
       }
       if (r < r_beg + w - 1) continue;  // window not yet complete
       const int64_t i = r - (w - 1);
+      // P[u] = sum_{c < u} V[c] at word u + u / 32; lane writes u = lane E + k + 1
       {
         auto vcol = [&](int k) -> VT {
           if constexpr (PACK) {
@@ -371,8 +396,10 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           run = add(run, vcol(k));
-          sm.p[wbase + k] = run;
+          const int u = ubase + k;
+          sm.p[u + (u >> 5)] = run;
         }
+        if (lane == 0) sm.p[0] = VT(0);
       }
       if constexpr (SQ) {
         VQ tot = VQ(0);
@@ -382,29 +409,43 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           run = add(run, Vq[k]);
-          sm.pq[wbase + k] = run;
+          const int u = ubase + k;
+          sm.pq[u + (u >> 5)] = run;
         }
+        if (lane == 0) sm.pq[0] = VQ(0);
       }
       __syncwarp();
-      const int64_t obase = i * o.ld + oc0;
-      for (int j = lane; j < nout; j += 32) {
-        const int ta = j - 1, tb = j + w - 1;  // inclusive prefixes P[j] = Pin[j-1], P[j+w] = Pin[j+w-1]
-        const int qa = ta + ta / E, qb = tb + tb / E;
-        const VT pa = (j == 0) ? VT(0) : sm.p[qa];
-        const VT sv = sub(sm.p[qb], pa);
-        VQ qv = VQ(0);
-        if constexpr (SQ) qv = sub(sm.pq[qb], (j == 0) ? VQ(0) : sm.pq[qa]);
-        if constexpr (kFloat) {
-          if (g.mask & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + obase + j, (double)sv);
-          if (g.mask & ST_MEAN) st_cs(o.mean + obase + j, fin_mean_f((double)sv, fi.dn));
-          if (g.mask & ST_STD) st_cs(o.std_ + obase + j, fin_std_f((double)sv, (double)qv, fi.dn));
-        } else {
-          uint64_t s64, q64 = 0;
-          if constexpr (sizeof(VT) == 4) s64 = (uint64_t)(uint32_t)sv; else s64 = (uint64_t)sv;
-          if constexpr (SQ) { if constexpr (sizeof(VQ) == 4) q64 = (uint64_t)(uint32_t)qv; else q64 = (uint64_t)qv; }
-          if (g.mask & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + obase + j, s64);
-          if (g.mask & ST_MEAN) st_cs(o.mean + obase + j, fin_mean_int(s64, fi));
-          if (g.mask & ST_STD) st_cs(o.std_ + obase + j, fin_std_int(s64, q64, fi));
+      // out[j] = P[j + w] - P[j], j = lane + 32 q: both words advance by 33 per q
+      const int64_t obase = i * o.ld + oc0 + lane;
+      const int nq = (nout - lane + 31) >> 5;
+      if (!kFloat && !SQ && g.mask == ST_SUM) {
+        uint64_t* dst = reinterpret_cast<uint64_t*>(o.sum) + obase;
+        int a = addr_a, bw = addr_b;
+#pragma unroll 4
+        for (int qq = 0; qq < nq; ++qq, a += 33, bw += 33, dst += 32) {
+          const VT sv = sub(sm.p[bw], sm.p[a]);
+          if constexpr (sizeof(VT) == 4) st_cs(dst, (uint64_t)(uint32_t)sv);
+          else st_cs(dst, (uint64_t)sv);
+        }
+      } else {
+        int a = addr_a, bw = addr_b;
+        for (int qq = 0; qq < nq; ++qq, a += 33, bw += 33) {
+          const int64_t at = obase + 32 * qq;
+          const VT sv = sub(sm.p[bw], sm.p[a]);
+          VQ qv = VQ(0);
+          if constexpr (SQ) qv = sub(sm.pq[bw], sm.pq[a]);
+          if constexpr (kFloat) {
+            if (g.mask & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + at, (double)sv);
+            if (g.mask & ST_MEAN) st_cs(o.mean + at, fin_mean_f((double)sv, fi.dn));
+            if (g.mask & ST_STD) st_cs(o.std_ + at, fin_std_f((double)sv, (double)qv, fi.dn));
+          } else {
+            uint64_t s64, q64 = 0;
+            if constexpr (sizeof(VT) == 4) s64 = (uint64_t)(uint32_t)sv; else s64 = (uint64_t)sv;
+            if constexpr (SQ) { if constexpr (sizeof(VQ) == 4) q64 = (uint64_t)(uint32_t)qv; else q64 = (uint64_t)qv; }
+            if (g.mask & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + at, s64);
+            if (g.mask & ST_MEAN) st_cs(o.mean + at, fin_mean_int(s64, fi));
+            if (g.mask & ST_STD) st_cs(o.std_ + at, fin_std_int(s64, q64, fi));
+          }
         }
       }
       __syncwarp();
