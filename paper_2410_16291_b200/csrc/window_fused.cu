@@ -20,6 +20,10 @@
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
 
+#ifndef SSB_FUSED_MINB
+#define SSB_FUSED_MINB 3
+#endif
+
 namespace ssb {
 
 template <typename InT, int E>
@@ -261,7 +265,7 @@ struct StripSmem {
 };
 
 template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ, bool PACK>
-__global__ void __launch_bounds__(32 * kStripWarps, 3)
+__global__ void __launch_bounds__(32 * kStripWarps, SSB_FUSED_MINB)
 fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeInt fi, int nJ, int nK,
                    int* __restrict__ nonfinite) {
   using SM = StripSmem<InT, E, RB, VT, VQ, SQ>;

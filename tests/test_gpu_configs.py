@@ -145,3 +145,24 @@ def test_c5_full_image(sb, hashes, dev):
     assert bool(torch.equal(fused, out))
     del out, fused, x
     torch.cuda.empty_cache()
+
+
+def test_u16_std_beyond_u64_squared_table(sb, dev):
+    """uint16 std on a 4.48 Gpx raster: the squared table exceeds 2^64 (the reference's
+    U128 arm, integral.py:44-55) and wraps modulo 2^64 on the device; window results
+    stay exact.  Checked on random output rows against the oracle's band evaluation."""
+    import torch
+
+    rows, cols, w = 70000, 64000, 16
+    assert sb.select_accum(sb.ElemKind.U16, rows, cols, True) is sb.AccumKind.U128
+    g = torch.Generator(device=dev)
+    g.manual_seed(16)
+    x = torch.randint(0, 65536, (rows, cols), dtype=torch.int32, device=dev, generator=g).to(torch.uint16)
+    res = sb.swa_stats(x, w, ("std", "sum"), pipeline="table")
+    rng = np.random.default_rng(16)
+    for i in [0, rows - w] + rng.integers(0, rows - w + 1, size=3).tolist():
+        band = host(x[i:i + w], np.uint16)
+        np.testing.assert_array_equal(host(res["std"][i], np.float64), O.swa(band, w, "std")[0])
+        np.testing.assert_array_equal(host(res["sum"][i], np.uint64), O.swa(band, w, "sum")[0])
+    del res, x
+    torch.cuda.empty_cache()
