@@ -50,12 +50,25 @@ def storage_dtype(np_dtype: np.dtype):
     }[np.dtype(np_dtype)]
 
 
+_TOTAL: dict = {}
+
+
+def total_memory(device) -> int:
+    """Device capacity, cached: cudaMemGetInfo can stall the host for tens of
+    milliseconds, so it stays off the per-call path."""
+    t = torch()
+    idx = t.device(device).index
+    idx = t.cuda.current_device() if idx is None else idx
+    if idx not in _TOTAL:
+        _TOTAL[idx] = int(t.cuda.get_device_properties(idx).total_memory)
+    return _TOTAL[idx]
+
+
 def empty(shape, np_dtype, device, what: str):
     """Device allocation that raises ResourceLimitError (integral.py:76-83) on failure."""
     t = torch()
     nbytes = int(np.prod(shape, dtype=object)) * np.dtype(np_dtype).itemsize
-    free, total = t.cuda.mem_get_info(device)
-    if nbytes > total:
+    if nbytes > total_memory(device):
         raise ResourceLimitError(nbytes, what)
     try:
         return t.empty(tuple(int(s) for s in shape), dtype=storage_dtype(np_dtype), device=device)

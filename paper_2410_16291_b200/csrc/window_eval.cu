@@ -226,10 +226,14 @@ constexpr int kTmaMaxNS = 8;  // pipeline depth (runtime, <= 8)
 // corner row is still in L2 when it is needed as a top corner row w rows later
 // (a static assignment lets CTAs drift apart and doubled the table reads).
 //
-// Item = (panel p, bottom table row rb, window k, chunk c): output row
-// rb - w_k of window k.  With several windows (multi_window, integral.py:199-210)
-// all windows that use table row rb as their bottom row are evaluated back to
-// back, so every table byte comes from HBM about once for the whole window set.
+// Item = (panel p, bottom table row rb, chunk c).  The stage holds the bottom
+// row segment once and one top row segment per window whose output row
+// rb - w_k exists, so with several windows (multi_window,
+// integral.py:199-210) the shared bottom row crosses L2->SM once instead of
+// once per window.  The sweep is bound by L2 throughput (~12 TB/s for hits,
+// misses and the output stream together), so bytes moved into shared memory
+// are what this layout minimises; every table byte comes from HBM about once
+// for the whole window set.
 __device__ unsigned long long g_eval_tickets[256];
 
 constexpr int kMaxWin = 8;
@@ -244,6 +248,10 @@ struct MultiEval {
   uint64_t n[kMaxWin];
   double dn[kMaxWin];
   unsigned char u64_ok[kMaxWin];
+  // stage layout (elements, per table): bottom segment at 0, top segment of
+  // window k at off[k]; a stage is NT * stage_elems elements
+  int off[kMaxWin];
+  int stage_elems;
 };
 
 template <typename Acc> struct FinK;
@@ -258,25 +266,30 @@ template <> struct FinK<double> {
   __device__ static Fin<double> make(const MultiEval& m, int k) { return Fin<double>{m.dn[k]}; }
 };
 
+// even number of elements covering [j0, j0 + CW + w) (reads reach index CW - 1 + w)
+__host__ __device__ __forceinline__ int64_t seg_need(int64_t cw, int64_t w) { return (cw + w + 1) & ~int64_t(1); }
+
 template <typename Acc, bool SQ, int U, bool MULTI>
 __global__ void __launch_bounds__(kThreads + 32)
 window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, const __grid_constant__ MultiEval g,
-                       int64_t seg, unsigned long long* __restrict__ ticket, int NS, int batch) {
+                       unsigned long long* __restrict__ ticket, int NS, int batch) {
   constexpr int NT = SQ ? 2 : 1;
-  constexpr int kTmaCW = kThreads * U;  // outputs per item
+  constexpr int kTmaCW = kThreads * U;  // output columns per item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + kTmaMaxNS;
-  // per stage: decoded item (output row i, -1 done, -2 skip), first column j0, window k
+  // per stage: bottom table row (-1 done, -2 skip), first column j0, window mask
   int64_t* meta = reinterpret_cast<int64_t*>(empty + kTmaMaxNS);
   int64_t* meta_j0 = meta + kTmaMaxNS;
-  int* meta_k = reinterpret_cast<int*>(meta_j0 + kTmaMaxNS);
-  Acc* buf = reinterpret_cast<Acc*>(smem_raw + 384);              // [NS][NT][2][seg]
+  int* meta_mask = reinterpret_cast<int*>(meta_j0 + kTmaMaxNS);
+  Acc* buf = reinterpret_cast<Acc*>(smem_raw + 384);              // [NS][NT][stage_elems]
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ld = g.sat_ld;
+  const int nwin = MULTI ? g.nwin : 1;
+  const int64_t stage_stride = (int64_t)NT * g.stage_elems;
   const int64_t nrb = g.R + 1 - g.wmin;  // bottom rows wmin..R
-  const int64_t per_panel = nrb * g.nwin * g.cpp;
-  const int64_t total = per_panel * (g.n_panels - 1) + nrb * g.nwin * g.cpl;
+  const int64_t per_panel = nrb * g.cpp;
+  const int64_t total = per_panel * (g.n_panels - 1) + nrb * g.cpl;
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
@@ -285,42 +298,43 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
     fence_mbar_init();
   }
   __syncthreads();
-  // item -> (output row i, window k, first column j0); false if the item maps to
-  // no output.  32-bit arithmetic (item counts stay far below 2^31).
-  const uint32_t ppan = (uint32_t)per_panel, cppf = (uint32_t)g.cpp, cppl = (uint32_t)g.cpl;
-  auto coords = [&](int64_t it64, int64_t& i, int& k, int64_t& j0) -> bool {
-    const uint32_t it = (uint32_t)it64;
-    const uint32_t p = it / ppan;
-    const uint32_t rem = it - p * ppan;
-    const uint32_t cpp = ((int64_t)p == g.n_panels - 1) ? cppl : cppf;
-    uint32_t rb_off, c;
-    if constexpr (MULTI) {
-      const uint32_t per_row = (uint32_t)g.nwin * cpp;
-      rb_off = rem / per_row;
-      const uint32_t rem2 = rem - rb_off * per_row;
-      k = (int)(rem2 / cpp);
-      c = rem2 - (uint32_t)k * cpp;
-    } else {
-      rb_off = rem / cpp;
-      k = 0;
-      c = rem - rb_off * cpp;
-    }
-    j0 = (int64_t)p * g.pw + (int64_t)c * kTmaCW;
-    i = (int64_t)rb_off + g.wmin - g.w[k];
-    return i >= 0 && i < g.out_r[k] && j0 < g.out_c[k];
-  };
   // warp 8 is the producer (one elected lane); warps 0-7 consume
   if (tid >= kThreads) {
     if (lane != 0) return;
     int64_t cur = 0, cur_end = 0;
     int64_t next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+    // decoded position of `cur`: full decode at the start of a ticket batch,
+    // then a carry-propagating increment (no divisions on the issue path).
+    // 32-bit arithmetic: item counts stay far below 2^31.
+    const uint32_t ppan = (uint32_t)per_panel, cppf = (uint32_t)g.cpp, cppl = (uint32_t)g.cpl;
+    const uint32_t nrb32 = (uint32_t)nrb;
+    uint32_t dp = 0, drb = 0, dc = 0, dcpp = 0;
+    auto decode = [&](int64_t it64) {
+      const uint32_t it = (uint32_t)it64;
+      dp = it / ppan;
+      const uint32_t rem = it - dp * ppan;
+      dcpp = ((int64_t)dp == g.n_panels - 1) ? cppl : cppf;
+      drb = rem / dcpp;
+      dc = rem - drb * dcpp;
+    };
+    auto advance = [&]() {
+      if (++dc < dcpp) return;
+      dc = 0;
+      if (++drb < nrb32) return;
+      drb = 0;
+      ++dp;
+      dcpp = ((int64_t)dp == g.n_panels - 1) ? cppl : cppf;
+    };
+    uint32_t s = 0, phase = 0;
     for (int64_t m = 0;; ++m) {
-      const int s = (int)(m % NS);
-      if (m >= NS) mbar_wait(&empty[s], (uint32_t)(((m / NS) - 1) & 1));
+      if (m >= NS) mbar_wait(&empty[s], phase ^ 1u);
       if (cur == cur_end) {  // tickets come in batches; the next batch is requested ahead
         cur = next_b;
         cur_end = next_b + batch;
         if (cur < total) next_b = (int64_t)atomicAdd(ticket, (unsigned long long)batch);
+        if (cur < total) decode(cur);
+      } else {
+        advance();
       }
       const int64_t it = cur++;
       if (it >= total) {
@@ -328,73 +342,89 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
         mbar_arrive_expect_tx(&full[s], 0);
         return;
       }
-      int64_t i, j0;
-      int k;
-      if (!coords(it, i, k, j0)) {
+      const int64_t rb = (int64_t)drb + g.wmin;
+      const int64_t j0 = (int64_t)dp * g.pw + (int64_t)dc * kTmaCW;
+      const int64_t avail = ld - j0;
+      int mask = 0;
+      int64_t wv = 0;
+      uint32_t bytes = 0;
+      for (int k = 0; k < nwin; ++k) {
+        if (rb >= g.w[k] && j0 < g.out_c[k]) {  // output row rb - w_k exists, chunk inside its columns
+          mask |= 1 << k;
+          wv = g.w[k] > wv ? g.w[k] : wv;
+          const int64_t len = seg_need(kTmaCW, g.w[k]);
+          bytes += (uint32_t)((len < avail ? len : avail) * 8);
+        }
+      }
+      if (mask == 0) {
         meta[s] = -2;
         mbar_arrive_expect_tx(&full[s], 0);
-        continue;
+      } else {
+        meta[s] = rb;
+        meta_j0[s] = j0;
+        meta_mask[s] = mask;
+        const int64_t lb = seg_need(kTmaCW, wv);
+        const uint32_t bb = (uint32_t)((lb < avail ? lb : avail) * 8);
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&full[s], (bytes + bb) * NT);
+        Acc* b = buf + (int64_t)s * stage_stride;
+        bulk_g2s(b, sat + rb * ld + j0, bb, &full[s]);
+        if constexpr (SQ) bulk_g2s(b + g.stage_elems, sq + rb * ld + j0, bb, &full[s]);
+        for (int k = 0; k < nwin; ++k) {
+          if (!((mask >> k) & 1)) continue;
+          const int64_t len = seg_need(kTmaCW, g.w[k]);
+          const uint32_t tb = (uint32_t)((len < avail ? len : avail) * 8);
+          const int64_t top = (rb - g.w[k]) * ld + j0;
+          bulk_g2s(b + g.off[k], sat + top, tb, &full[s]);
+          if constexpr (SQ) bulk_g2s(b + g.stage_elems + g.off[k], sq + top, tb, &full[s]);
+        }
       }
-      meta[s] = i;
-      meta_j0[s] = j0;
-      meta_k[s] = k;
-      const int64_t w = g.w[k];
-      const int64_t need = (kTmaCW + w + 1) & ~int64_t(1);
-      int64_t len = ld - j0 < need ? ld - j0 : need;
-      len &= ~int64_t(1);
-      const uint32_t bytes = (uint32_t)(len * 8);
-      fence_proxy_async();
-      mbar_arrive_expect_tx(&full[s], bytes * 2 * NT);
-      Acc* b = buf + (int64_t)s * NT * 2 * seg;
-      bulk_g2s(b, sat + i * ld + j0, bytes, &full[s]);
-      bulk_g2s(b + seg, sat + (i + w) * ld + j0, bytes, &full[s]);
-      if constexpr (SQ) {
-        bulk_g2s(b + 2 * seg, sq + i * ld + j0, bytes, &full[s]);
-        bulk_g2s(b + 3 * seg, sq + (i + w) * ld + j0, bytes, &full[s]);
-      }
+      if (++s == (uint32_t)NS) { s = 0; phase ^= 1u; }
     }
   }
-  for (int64_t m = 0;; ++m) {
-    const int s = (int)(m % NS);
-    mbar_wait(&full[s], (uint32_t)((m / NS) & 1));
-    const int64_t i = meta[s];
-    if (i == -1) break;
-    if (i == -2) {
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
-      continue;
-    }
-    const int64_t j0 = meta_j0[s];
-    const int k = meta_k[s];
-    const int64_t w = g.w[k];
-    const Acc* T = buf + (int64_t)s * NT * 2 * seg;
-    const Acc* B = T + seg;
-    Acc sv[U], qv[U];
+  uint32_t s = 0, phase = 0;
+  for (;;) {
+    mbar_wait(&full[s], phase);
+    const int64_t rb = meta[s];
+    if (rb == -1) break;
+    if (rb != -2) {
+      const int64_t j0 = meta_j0[s];
+      const int mask = meta_mask[s];
+      const Acc* B = buf + (int64_t)s * stage_stride;
+#pragma unroll 1
+      for (int k = 0; k < nwin; ++k) {
+        if (!((mask >> k) & 1)) continue;
+        const int w = (int)g.w[k];
+        const Acc* T = B + g.off[k];
+        Acc sv[U], qv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int jj = tid + kThreads * u;
-      sv[u] = corner4<Acc>(B[jj + w], T[jj + w], B[jj], T[jj]);
-      if constexpr (SQ) {
-        const Acc* TQ = T + 2 * seg;
-        const Acc* BQ = T + 3 * seg;
-        qv[u] = corner4<Acc>(BQ[jj + w], TQ[jj + w], BQ[jj], TQ[jj]);
+        for (int u = 0; u < U; ++u) {
+          const int jj = tid + kThreads * u;
+          sv[u] = corner4<Acc>(B[jj + w], T[jj + w], B[jj], T[jj]);
+          if constexpr (SQ) {
+            const Acc* BQ = B + g.stage_elems;
+            const Acc* TQ = T + g.stage_elems;
+            qv[u] = corner4<Acc>(BQ[jj + w], TQ[jj + w], BQ[jj], TQ[jj]);
+          }
+        }
+        const WinOut& o = g.o[k];
+        const Fin<Acc> fin = FinK<Acc>::make(g, k);
+        const int64_t base = (rb - w) * o.ld + j0;
+        const int64_t oc = g.out_c[k] - j0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int jj = tid + kThreads * u;
+          if (jj >= oc) break;
+          const int64_t at = base + jj;
+          if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, sv[u]);
+          if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(sv[u]));
+          if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(sv[u], qv[u]));
+        }
       }
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
-    const WinOut& o = g.o[k];
-    const Fin<Acc> fin = FinK<Acc>::make(g, k);
-    const int64_t base = i * o.ld + j0;
-    const int64_t oc = g.out_c[k];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + tid + kThreads * u;
-      if (j >= oc) break;
-      const int64_t at = base + tid + kThreads * u;
-      if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, sv[u]);
-      if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(sv[u]));
-      if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(sv[u], qv[u]));
-    }
+    if (++s == (uint32_t)NS) { s = 0; phase ^= 1u; }
   }
 }
 
@@ -414,21 +444,28 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   used = false;
   constexpr int NT = SQ ? 2 : 1;
   constexpr int64_t kTmaCW = kThreads * U;
-  const int64_t seg = (kTmaCW + m.wmax + 1) & ~int64_t(1);
   const char* env_b = getenv("SSB_EVAL_BATCH");
   const int batch = env_b ? atoi(env_b) : 4;
   const char* env_ns = getenv("SSB_EVAL_STAGES");
   int NS = env_ns ? atoi(env_ns) : 3;
   if (NS < 2) NS = 2;
   if (NS > kTmaMaxNS) NS = kTmaMaxNS;
-  const size_t smem = 384 + (size_t)NS * NT * 2 * seg * sizeof(Acc);
-  if (smem > 200 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) ||
+  // stage layout: bottom segment (covers the widest window), then one top
+  // segment per window; every segment an even element count (16-byte aligned)
+  int64_t el = seg_need(kTmaCW, m.wmax);
+  for (int k = 0; k < m.nwin; ++k) {
+    m.off[k] = (int)el;
+    el += seg_need(kTmaCW, m.w[k]);
+  }
+  m.stage_elems = (int)el;
+  const size_t smem = 384 + (size_t)NS * NT * el * sizeof(Acc);
+  if (smem > 220 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) ||
       (SQ && (reinterpret_cast<uintptr_t>(sat_sq) & 15)) || (m.sat_ld & 1))
     return cudaSuccess;
   const char* env_mb = getenv("SSB_EVAL_L2_MB");
   int64_t out_c_max = 0;
   for (int k = 0; k < m.nwin; ++k) out_c_max = m.out_c[k] > out_c_max ? m.out_c[k] : out_c_max;
-  // multi-window keeps wmax rows of every window's panel hot; scale the budget
+  // the panel's wmax + 1 most recent table rows stay hot in L2
   const double mb = env_mb ? atof(env_mb) : 8.0;
   m.pw = panel_width_max(out_c_max, m.wmax, SQ, kTmaCW, mb * 1024 * 1024);
   m.n_panels = (out_c_max + m.pw - 1) / m.pw;
@@ -452,13 +489,18 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   kfn<<<blocks, kThreads + 32, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq),
-                                           m, seg, ticket, NS, batch);
+                                           m, ticket, NS, batch);
   used = true;
   return cudaGetLastError();
 }
 
 template <typename Acc, bool SQ>
 cudaError_t launch_tma_multi(const void* sat, const void* sat_sq, const MultiEval& m, cudaStream_t st, bool& used) {
+  // multi-window stages hold one top segment per window: narrower chunks keep
+  // two CTAs per SM resident (tuning: SSB_EVAL_U=2|4)
+  const char* env_u = getenv("SSB_EVAL_U");
+  const int u = env_u ? atoi(env_u) : (m.nwin > 2 ? 2 : 4);
+  if (u == 2) return launch_tma_multi_u<Acc, SQ, 2>(sat, sat_sq, m, st, used);
   return launch_tma_multi_u<Acc, SQ, 4>(sat, sat_sq, m, st, used);
 }
 

@@ -14,6 +14,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2410_16291_b200 as sb  # noqa: E402
 from paper_2410_16291_b200 import _device, synthetic  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6443.2
 dev = torch.device("cuda", 0)
@@ -54,7 +55,8 @@ def main():
                 fn = lambda: sb.swa_stats(x, w, cfg.stats, pipeline=pipe)  # noqa: E731
                 outs = len(cfg.stats) * (R - w + 1) * (C - w + 1) * 8
             try:
-                ms = timeit(fn, reps=3 if name in ("C3", "C5") else 5)
+                with ClockSampler(0) as clk:
+                    ms = timeit(fn, reps=int(os.environ.get("REPS", 3 if name in ("C3", "C5") else 5)))
             except Exception as exc:  # pragma: no cover
                 print(json.dumps({"config": name, "pipeline": pipe, "error": str(exc)}), flush=True)
                 continue
@@ -63,7 +65,8 @@ def main():
             print(json.dumps({"config": name, "pipeline": pipe, "ms": round(ms, 3),
                               "gpx_s": round(R * C / ms / 1e6, 1), "alg_GB": round(bytes_ / 1e9, 2),
                               "roofline_frac": round(bytes_ / ms / 1e6 / PEAK, 3), "gen_s": round(gen, 1),
-                              "alloc_retries": torch.cuda.memory_stats().get("num_alloc_retries", 0)}), flush=True)
+                              "alloc_retries": torch.cuda.memory_stats().get("num_alloc_retries", 0),
+                              "clocks": clk.summary()}), flush=True)
             torch.cuda.empty_cache()
         del x
         torch.cuda.empty_cache()
