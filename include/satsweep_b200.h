@@ -18,6 +18,10 @@
  *   ssb_window_sum_at    window_sum (integral.py:119-130)
  *   ssb_swa_host         api.swa with host buffers (api.py:28-55): host->device
  *                        copies, compute, device->host copies, streamed by bands
+ *   ssb_file_to_device   the payload read of read_pgm / read_raw
+ *                        (imgio.py:72-103, :160-174) straight into device memory
+ *   ssb_device_to_file   the payload write of write_pgm / write_raw
+ *                        (imgio.py:106-116, :127-139) straight from device memory
  *
  * Conventions
  *   - Device rasters must be 16-byte aligned (rows are staged with TMA bulk
@@ -140,6 +144,28 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
 
 /* Count of kernel launches the library issued since load (diagnostics). */
 int64_t ssb_launch_count(void);
+
+/* File front door.  Copy `nbytes` at byte `offset` of the
+ * file at `path` into device memory `dst`, streamed through pinned staging
+ * with parallel reads overlapped with the host->device copies.  swap16 != 0
+ * byte-swaps 16-bit samples on the device afterwards (big-endian PGM); it
+ * needs an even `nbytes` and a 16-byte aligned `dst`.  The file must hold at
+ * least offset + nbytes bytes (SSB_EINVAL otherwise).  Synchronises `stream`.
+ * Replaces the payload half of imgio.read_pgm / read_raw (imgio.py:93-103,
+ * :169-174); header parsing and its error messages stay in the facade. */
+int ssb_file_to_device(const char* path, int64_t offset, int64_t nbytes, void* dst, int swap16, void* stream);
+
+/* Sets *flag (device int, caller-zeroed) to 1 if any of the n floats at `x`
+ * is NaN or +-Inf: the finiteness rule of ImageGrid (grid.py:82-83) for rasters
+ * that arrive on the device without a host copy.  Asynchronous on `stream`. */
+int ssb_f32_nonfinite(const void* x, int64_t n, int* flag, void* stream);
+
+/* Write `nbytes` of device memory `src` into the file at `path` starting at
+ * byte `offset` (created if absent, sized to offset + nbytes; bytes before
+ * `offset`, e.g. a PGM header, are kept).  swap16 != 0 writes 16-bit samples
+ * big-endian (the source is not modified).  Synchronises `stream`.  Replaces
+ * the payload half of imgio.write_pgm / write_raw (imgio.py:106-116, :127-139). */
+int ssb_device_to_file(const char* path, int64_t offset, const void* src, int64_t nbytes, int swap16, void* stream);
 
 #ifdef __cplusplus
 }

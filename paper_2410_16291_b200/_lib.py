@@ -48,6 +48,9 @@ _SIGS = {
     "ssb_window_fused": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _i64, _vp, _int, _vp]),
     "ssb_window_sum_at": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "ssb_swa_host": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _i64, _int, _int, _i64]),
+    "ssb_file_to_device": (_int, [ctypes.c_char_p, _i64, _i64, _vp, _int, _vp]),
+    "ssb_device_to_file": (_int, [ctypes.c_char_p, _i64, _vp, _i64, _int, _vp]),
+    "ssb_f32_nonfinite": (_int, [_vp, _i64, _vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
 

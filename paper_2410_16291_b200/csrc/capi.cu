@@ -37,6 +37,7 @@ constexpr int64_t kFusedMaxWindow = 3072;
 
 static std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int io_fail(int code, const char* fmt, ...);
 }  // namespace ssb
 
 using namespace ssb;
@@ -92,6 +93,17 @@ int check_stats(int dtype, int mask) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 }  // namespace
+
+// io.cu reports through the same thread-local message
+int ssb::io_fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
 
 extern "C" {
 
