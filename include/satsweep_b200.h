@@ -112,6 +112,20 @@ int ssb_window_eval(const void* sat, const void* sat_sq, int in_dtype, int64_t r
                     int64_t w, int64_t stride, int stat_mask, void* out_sum, double* out_mean, double* out_std,
                     int64_t out_ld, void* stream);
 
+/* Same contract and bit-identical result as ssb_sat_build, computed by the
+ * single-pass kernel: each pixel read once, each entry written once, carries
+ * between tiles by decoupled look-back (north_star subsystem 1).  Integer
+ * input only (u8, u16, i32 without squares; SSB_EUNSUPPORTED otherwise).
+ * Slower than the default reduce-then-scan build at BASELINE C5 on B200
+ * (DESIGN.md section 3), so ssb_sat_build does not route here unless the
+ * environment variable SSB_SAT_PATH=one is set.  Its workspace (tile flags and
+ * published aggregates) is sized by ssb_sat_lookback_workspace_bytes (-1 for
+ * unsupported requests). */
+int64_t ssb_sat_lookback_workspace_bytes(int in_dtype, int64_t rows, int64_t cols, int with_squares);
+int ssb_sat_build_lookback(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                           void* sat_sq, int64_t sat_ld, const void* carry, const void* carry_sq, void* ws,
+                           int64_t ws_bytes, void* stream);
+
 /* Several window sizes (stride 1) from one set of tables. */
 int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols,
                           int64_t sat_ld, int n_windows, const int64_t* windows, int stat_mask,

@@ -10,12 +10,14 @@ several threads run concurrently, as the reference's numpy kernels did
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import GridValidationError, InvalidWindowError, ResourceLimitError, SatsweepError
 
-LIB_PATH = Path(__file__).resolve().parent / "libsatsweep_b200.so"
+LIB_PATH = Path(os.environ["SSB_LIB"]) if os.environ.get("SSB_LIB") else (
+    Path(__file__).resolve().parent / "libsatsweep_b200.so")  # SSB_LIB: tuning builds only
 
 # status codes / enums (include/satsweep_b200.h)
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED, ENONFINITE = 0, 1, 2, 3, 4, 5
@@ -39,6 +41,8 @@ _SIGS = {
     "ssb_sat_prepare": (_int, [_vp, _int, _i64, _i64, _i64, _int, _vp, _i64, _vp, _vp, _vp, _vp]),
     "ssb_sat_finish": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp]),
     "ssb_sat_build": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "ssb_sat_lookback_workspace_bytes": (_i64, [_int, _i64, _i64, _int]),
+    "ssb_sat_build_lookback": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp]),
     "ssb_window_eval": (_int, [_vp, _vp, _int, _i64, _i64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _i64, _vp]),
     "ssb_window_eval_multi": (
         _int,

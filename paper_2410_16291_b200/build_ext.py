@@ -36,24 +36,26 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: Path | None = None) -> Path:
+    """``defines``/``lib``: tuning variants (e.g. SSB_ONEPASS_PROF) built next to, never over, the product library."""
+    target = lib or LIB
+    if not force and not defines and lib is None and not _stale():
         return LIB
-    out_dir = PKG / "_build"
+    out_dir = PKG / ("_build" if not defines else "_build_variant")
     out_dir.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = out_dir / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     subprocess.run([nvcc(), *ARCH, "-shared", *objs, "-o", str(tmp), "-cudart", "static"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

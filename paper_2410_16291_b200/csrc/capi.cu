@@ -25,6 +25,13 @@ cudaError_t launch_sat_prepare(int dtype, const void* in, int64_t R, int64_t C, 
 cudaError_t launch_sat_finish(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, void* sat_sq,
                               int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, cudaStream_t st);
 int64_t sat_workspace_bytes(int dtype, int64_t R, int64_t C, bool sq);
+cudaError_t launch_sat_onepass(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, void* sat_sq,
+                               int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, cudaStream_t st);
+bool onepass_supported(int dtype, bool sq);
+int64_t sat_onepass_workspace_bytes(int dtype, int64_t R, int64_t C, bool sq);
+cudaError_t launch_sat_build(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, void* sat_sq,
+                             int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, int* nonfinite,
+                             cudaStream_t st);
 void sat_plan_info(int dtype, int64_t R, int64_t C, bool sq, int64_t* info);
 cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R, int64_t C,
                                int64_t sat_ld, int64_t w, int64_t s, int mask, WinOut o, cudaStream_t st);
@@ -117,6 +124,11 @@ int64_t ssb_sat_workspace_bytes(int in_dtype, int64_t rows, int64_t cols, int wi
   return sat_workspace_bytes(in_dtype, rows, cols, with_squares != 0);
 }
 
+int64_t ssb_sat_lookback_workspace_bytes(int in_dtype, int64_t rows, int64_t cols, int with_squares) {
+  if (!valid_dtype(in_dtype) || rows < 1 || cols < 1 || !onepass_supported(in_dtype, with_squares != 0)) return -1;
+  return sat_onepass_workspace_bytes(in_dtype, rows, cols, with_squares != 0);
+}
+
 int ssb_sat_plan(int in_dtype, int64_t rows, int64_t cols, int with_squares, int64_t* info4) {
   if (!valid_dtype(in_dtype) || rows < 1 || cols < 1 || !info4) return fail(SSB_EINVAL, "bad plan request");
   sat_plan_info(in_dtype, rows, cols, with_squares != 0, info4);
@@ -156,10 +168,38 @@ int ssb_sat_finish(const void* in, int in_dtype, int64_t rows, int64_t cols, int
 int ssb_sat_build(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat, void* sat_sq,
                   int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, int64_t ws_bytes,
                   int* nonfinite_flag, void* stream) {
-  int rc = ssb_sat_prepare(in, in_dtype, rows, cols, in_ld, sat_sq != nullptr, ws, ws_bytes, nullptr, nullptr,
-                           nonfinite_flag, stream);
+  int rc = check_image(in_dtype, rows, cols, in_ld);
   if (rc) return rc;
-  return ssb_sat_finish(in, in_dtype, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws, ws_bytes, stream);
+  if (in_dtype == SSB_I32 && sat_sq) return fail(SSB_EUNSUPPORTED, "squared tables are not supported for int32 input");
+  if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
+  if ((rc = check_aligned(in, "input raster"))) return rc;
+  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
+  if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
+    return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, sat_sq != nullptr);
+  if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  cudaError_t e = launch_sat_build(in_dtype, in, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws,
+                                   nonfinite_flag, as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build");
+}
+
+int ssb_sat_build_lookback(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                           void* sat_sq, int64_t sat_ld, const void* carry, const void* carry_sq, void* ws,
+                           int64_t ws_bytes, void* stream) {
+  int rc = check_image(in_dtype, rows, cols, in_ld);
+  if (rc) return rc;
+  if (!onepass_supported(in_dtype, sat_sq != nullptr))
+    return fail(SSB_EUNSUPPORTED, "the single-pass build takes integer input (no squares for int32)");
+  if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
+  if ((rc = check_aligned(in, "input raster"))) return rc;
+  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
+  if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
+    return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  const int64_t need = sat_onepass_workspace_bytes(in_dtype, rows, cols, sat_sq != nullptr);
+  if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  cudaError_t e = launch_sat_onepass(in_dtype, in, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws,
+                                     as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build_lookback");
 }
 
 int ssb_window_eval(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols, int64_t sat_ld,
@@ -356,9 +396,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
                                cudaMemcpyHostToDevice, s.st)) != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
     WinOut o{s.o_sum, reinterpret_cast<double*>(s.o_mean), reinterpret_cast<double*>(s.o_std), out_c};
     if (pipeline == SSB_PIPE_TABLE) {
-      e = launch_sat_prepare(in_dtype, s.in, nr, cols, cols, sq, s.ws, nullptr, nullptr, d_flag, s.st);
-      if (e == cudaSuccess)
-        e = launch_sat_finish(in_dtype, s.in, nr, cols, cols, s.sat, s.sq, sat_ld, nullptr, nullptr, s.ws, s.st);
+      e = launch_sat_build(in_dtype, s.in, nr, cols, cols, s.sat, s.sq, sat_ld, nullptr, nullptr, s.ws, d_flag, s.st);
       if (e == cudaSuccess)
         e = launch_window_eval(s.sat, s.sq, in_dtype == SSB_F32, in_dtype, nr, cols, sat_ld, w, stride, stat_mask, o, s.st);
     } else {

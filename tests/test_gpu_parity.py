@@ -360,3 +360,84 @@ def test_concurrent_threads(sb):
     for t in ts:
         t.join()
     assert not errs, errs
+
+
+# ---------------------------------------------------------------- single-pass look-back build
+@pytest.mark.parametrize("shape", [(1, 1), (1, 700), (700, 1), (129, 513), (127, 511), (1025, 1537), (3001, 4099)])
+@pytest.mark.parametrize("kind", ["u8", "u16", "i32"])
+def test_lookback_build_matches_oracle(sb, shape, kind):
+    """ssb_sat_build_lookback (single pass, decoupled look-back) vs the oracle:
+    plain, squared-only and both tables, with and without a carry row."""
+    import torch
+
+    from paper_2410_16291_b200 import _device, _engine, _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(hash(("lb", shape, kind)) % 2**32)
+    R, C = shape
+    if kind == "i32":
+        v = rng.integers(-(2**31), 2**31, size=shape, dtype=np.int64).astype(np.int32)
+    else:
+        v = random_values(rng, R, C, kind)
+    code = {"u8": _lib.U8, "u16": _lib.U16, "i32": _lib.I32}[kind]
+    x = to_dev(v)
+    ld = _engine.sat_ld_for(C)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream().cuda_stream
+    carry_h = rng.integers(0, 2**63, size=C + 1, dtype=np.uint64)
+    modes = [(True, False), (False, True), (True, True)] if kind != "i32" else [(True, False)]
+    for plain, sq in modes:
+        for with_carry in (False, True):
+            sat = _device.empty((R + 1, ld), np.uint64, dev, "t") if plain else None
+            sat_sq = _device.empty((R + 1, ld), np.uint64, dev, "t") if sq else None
+            wsb = int(lib.ssb_sat_lookback_workspace_bytes(code, R, C, 1 if sq else 0))
+            ws = _device.empty((wsb,), np.uint8, dev, "ws")
+            carry = to_dev(carry_h.view(np.int64)) if with_carry else None
+            ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+            _lib.check(lib.ssb_sat_build_lookback(x.data_ptr(), code, R, C, C, ptr(sat), ptr(sat_sq), ld, ptr(carry),
+                                                  ptr(carry), ws.data_ptr(), wsb, st))
+            torch.cuda.synchronize()
+            for tab, squared in ((sat, False), (sat_sq, True)):
+                if tab is None:
+                    continue
+                ref = O.build_table(v, squared).astype(np.uint64)
+                if with_carry:
+                    ref = ref + carry_h[None, :]  # wraps modulo 2^64 like the device table
+                got = host(tab, np.uint64)[:, : C + 1]
+                np.testing.assert_array_equal(got, ref)
+
+
+def test_lookback_build_refuses_float(sb):
+    from paper_2410_16291_b200 import _lib
+
+    lib = _lib.load()
+    rc = lib.ssb_sat_build_lookback(None, _lib.F32, 4, 4, 4, None, None, 6, None, None, None, 0, None)
+    assert rc == _lib.EUNSUPPORTED
+
+
+@pytest.mark.parametrize("kind", ["u8", "u16"])
+def test_lookback_build_large_matches_two_pass(sb, kind):
+    """12,000 x 30,001: thousands of tiles in flight, long look-back chains; bit-identical to the default build."""
+    import torch
+
+    from paper_2410_16291_b200 import _device, _engine, _lib
+
+    lib = _lib.load()
+    R, C = 12000, 30001
+    rng = np.random.default_rng(7)
+    v = rng.integers(0, 256 if kind == "u8" else 65536, size=(R, C), dtype=np.uint8 if kind == "u8" else np.uint16)
+    code = _lib.U8 if kind == "u8" else _lib.U16
+    x = to_dev(v)
+    ld = _engine.sat_ld_for(C)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream().cuda_stream
+    wsb = max(int(lib.ssb_sat_workspace_bytes(code, R, C, 0)), int(lib.ssb_sat_lookback_workspace_bytes(code, R, C, 0)))
+    ws = _device.empty((wsb,), np.uint8, dev, "ws")
+    a = _device.empty((R + 1, ld), np.uint64, dev, "t")
+    b = _device.empty((R + 1, ld), np.uint64, dev, "t")
+    _lib.check(lib.ssb_sat_build(x.data_ptr(), code, R, C, C, a.data_ptr(), None, ld, None, None, ws.data_ptr(), wsb,
+                                 None, st))
+    _lib.check(lib.ssb_sat_build_lookback(x.data_ptr(), code, R, C, C, b.data_ptr(), None, ld, None, None,
+                                          ws.data_ptr(), wsb, st))
+    torch.cuda.synchronize()
+    assert torch.equal(a[:, : C + 1], b[:, : C + 1])
