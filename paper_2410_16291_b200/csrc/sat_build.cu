@@ -212,8 +212,11 @@ __device__ __forceinline__ T warp_reduce_scatter(T (&v)[N], int lane) {
 
 // ---------------------------------------------------------------------------
 // phase 1
+#ifndef SSB_REDUCE_MINB
+#define SSB_REDUCE_MINB 3
+#endif
 template <typename InT, bool SQ, int RBR, int WPC>
-__global__ void __launch_bounds__(32 * WPC)
+__global__ void __launch_bounds__(32 * WPC, SQ ? 1 : SSB_REDUCE_MINB)
 sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                   typename Elem<InT>::Acc* __restrict__ rowtot, typename Elem<InT>::Acc* __restrict__ rowtot_sq,
                   typename Elem<InT>::Acc* __restrict__ colp, typename Elem<InT>::Acc* __restrict__ colp_sq,
@@ -285,8 +288,31 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
     // interior blocks (all RB rows are image rows) on interior lanes (all E
     // columns inside the image) take a check-free path
     const bool fast = lane_inside && nr == RB && r0 >= 1 && r0 + RB - 1 <= R;
+    if constexpr (kPacked && !SQ && (RB % 2) == 0) {
+      if (fast) {
+        // two rows at a time: byte pairs unpacked with LOP3 / PRMT, both rows
+        // folded into the 16-bit column partials by one 3-input add each
+#pragma unroll
+        for (int r = 0; r < RB; r += 2) {
+          uint32_t o1[NWD], o2[NWD];
+          lane_bytes<G::LB>(ws.buf[s] + r * G::ROWB, qbase + ws.offs[s][r], o1);
+          lane_bytes<G::LB>(ws.buf[s] + (r + 1) * G::ROWB, qbase + ws.offs[s][r + 1], o2);
+          part[r] = lane_total<InT>(o1);
+          part[r + 1] = lane_total<InT>(o2);
+#pragma unroll
+          for (int i = 0; i < NWD; ++i) {
+            pk_lo[i] += (o1[i] & 0x00FF00FFu) + (o2[i] & 0x00FF00FFu);
+            pk_hi[i] += __byte_perm(o1[i], 0u, 0x4341) + __byte_perm(o2[i], 0u, 0x4341);
+          }
+          part_sq[r] = part_sq[r + 1] = LocSq(0);
+        }
+      }
+    }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
+      if constexpr (kPacked && !SQ && (RB % 2) == 0) {
+        if (fast) continue;
+      }
       part[r] = Loc(0);
       part_sq[r] = LocSq(0);
       if (fast || r < nr) {
@@ -1134,7 +1160,14 @@ template <typename InT, bool SQ>
 cudaError_t launch_reduce_cfg(const InT* x, int64_t R, int64_t C, int64_t in_ld, typename Elem<InT>::Acc* rowtot,
                               typename Elem<InT>::Acc* rowtot_sq, typename Elem<InT>::Acc* colp,
                               typename Elem<InT>::Acc* colp_sq, int* nonfinite, cudaStream_t st, const SatPlan& p) {
-  return launch_reduce_rw<InT, SQ, 0, kWarpsPerCta>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq, nonfinite, st, p);
+#ifndef SSB_REDUCE_WPC
+#define SSB_REDUCE_WPC 8
+#endif
+#ifndef SSB_REDUCE_RB
+#define SSB_REDUCE_RB 0
+#endif
+  return launch_reduce_rw<InT, SQ, SSB_REDUCE_RB, SSB_REDUCE_WPC>(x, R, C, in_ld, rowtot, rowtot_sq, colp, colp_sq,
+                                                                  nonfinite, st, p);
 }
 
 template <typename InT, bool SQ>
