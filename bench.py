@@ -167,7 +167,7 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-rows", type=int, default=4096, help="output rows per reference/CPU step")
     ap.add_argument("--cpu-rows", type=int, default=16384, help="output rows of the cpu_baseline sample")
-    ap.add_argument("--cpu-reps", type=int, default=4, help="repetitions of the cpu_baseline sample (~10-30 s of CPU work)")
+    ap.add_argument("--cpu-reps", type=int, default=8, help="repetitions of the cpu_baseline sample (~10-30 s of CPU work)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--rows", type=int, default=ROWS, help="(debug) smaller image")
