@@ -272,7 +272,7 @@ __host__ __device__ __forceinline__ int64_t seg_need(int64_t cw, int64_t w) { re
 template <typename Acc, bool SQ, int U, bool MULTI>
 __global__ void __launch_bounds__(kThreads + 32)
 window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, const __grid_constant__ MultiEval g,
-                       unsigned long long* __restrict__ ticket, int NS, int batch) {
+                       unsigned long long* __restrict__ ticket, int NS, int batch, int hints) {
   constexpr int NT = SQ ? 2 : 1;
   constexpr int kTmaCW = kThreads * U;  // output columns per item
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -325,6 +325,7 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
       ++dp;
       dcpp = ((int64_t)dp == g.n_panels - 1) ? cppl : cppf;
     };
+    const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
     uint32_t s = 0, phase = 0;
     for (int64_t m = 0;; ++m) {
       if (m >= NS) mbar_wait(&empty[s], phase ^ 1u);
@@ -368,15 +369,28 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
         fence_proxy_async();
         mbar_arrive_expect_tx(&full[s], (bytes + bb) * NT);
         Acc* b = buf + (int64_t)s * stage_stride;
-        bulk_g2s(b, sat + rb * ld + j0, bb, &full[s]);
-        if constexpr (SQ) bulk_g2s(b + g.stage_elems, sq + rb * ld + j0, bb, &full[s]);
+        if (hints) {
+          // bottom rows come back as top rows w rows later: keep them in L2;
+          // a top row of the largest window is read for the last time
+          bulk_g2s_hint(b, sat + rb * ld + j0, bb, &full[s], pol_keep);
+          if constexpr (SQ) bulk_g2s_hint(b + g.stage_elems, sq + rb * ld + j0, bb, &full[s], pol_keep);
+        } else {
+          bulk_g2s(b, sat + rb * ld + j0, bb, &full[s]);
+          if constexpr (SQ) bulk_g2s(b + g.stage_elems, sq + rb * ld + j0, bb, &full[s]);
+        }
         for (int k = 0; k < nwin; ++k) {
           if (!((mask >> k) & 1)) continue;
           const int64_t len = seg_need(kTmaCW, g.w[k]);
           const uint32_t tb = (uint32_t)((len < avail ? len : avail) * 8);
           const int64_t top = (rb - g.w[k]) * ld + j0;
-          bulk_g2s(b + g.off[k], sat + top, tb, &full[s]);
-          if constexpr (SQ) bulk_g2s(b + g.stage_elems + g.off[k], sq + top, tb, &full[s]);
+          if (hints) {
+            const uint64_t pol = g.w[k] == g.wmax ? pol_drop : pol_keep;
+            bulk_g2s_hint(b + g.off[k], sat + top, tb, &full[s], pol);
+            if constexpr (SQ) bulk_g2s_hint(b + g.stage_elems + g.off[k], sq + top, tb, &full[s], pol);
+          } else {
+            bulk_g2s(b + g.off[k], sat + top, tb, &full[s]);
+            if constexpr (SQ) bulk_g2s(b + g.stage_elems + g.off[k], sq + top, tb, &full[s]);
+          }
         }
       }
       if (++s == (uint32_t)NS) { s = 0; phase ^= 1u; }
@@ -465,8 +479,11 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   const char* env_mb = getenv("SSB_EVAL_L2_MB");
   int64_t out_c_max = 0;
   for (int k = 0; k < m.nwin; ++k) out_c_max = m.out_c[k] > out_c_max ? m.out_c[k] : out_c_max;
-  // the panel's wmax + 1 most recent table rows stay hot in L2
-  const double mb = env_mb ? atof(env_mb) : 8.0;
+  // the panel's wmax + 1 most recent table rows stay hot in L2.  Single
+  // window: 16 MB panels with evict_last on bottom rows / evict_first on top
+  // rows (C5 sweep 15.14 -> 14.81 ms); the multi-window set measured best
+  // without policies at 8 MB.
+  const double mb = env_mb ? atof(env_mb) : (m.nwin == 1 ? 16.0 : 8.0);
   m.pw = panel_width_max(out_c_max, m.wmax, SQ, kTmaCW, mb * 1024 * 1024);
   m.n_panels = (out_c_max + m.pw - 1) / m.pw;
   m.cpp = m.pw / kTmaCW;
@@ -488,8 +505,10 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   unsigned long long* ticket = tickets + (slot.fetch_add(1) % 256);
   e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
+  const char* env_h = getenv("SSB_EVAL_TMA_HINTS");  // tuning: L2 policies on the table row copies
+  const int hints = env_h ? atoi(env_h) : (m.nwin == 1 ? 1 : 0);
   kfn<<<blocks, kThreads + 32, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq),
-                                           m, ticket, NS, batch);
+                                           m, ticket, NS, batch, hints);
   used = true;
   return cudaGetLastError();
 }
