@@ -35,7 +35,10 @@
 #include "ssb_stage.cuh"
 
 #ifndef SSB_SCAN_MINB
-#define SSB_SCAN_MINB 2
+#define SSB_SCAN_MINB 1
+#endif
+#ifndef SSB_SCAN_STAGES
+#define SSB_SCAN_STAGES 2
 #endif
 
 namespace ssb {
@@ -139,13 +142,14 @@ __device__ __forceinline__ bool any_nonfinite(const uint32_t* o) {
 // transpose and no CTA-wide barrier anywhere in the sweep.
 constexpr int kWarpsPerCta = kThreads / 32;
 
-template <typename InT, int RB_ = 0>
+template <typename InT, int RB_ = 0, int NSTG_ = 2>
 struct WarpStage {
   using G = Geo<InT>;
   static constexpr int RBW = RB_ > 0 ? RB_ : (G::ES == 1 ? 8 : 4);  // rows per stage (<= 32)
-  alignas(16) unsigned char buf[2][RBW * G::ROWB];
-  int offs[2][RBW];
-  uint64_t bar[2];
+  static constexpr int NSTG = NSTG_;                               // ring depth
+  alignas(16) unsigned char buf[NSTG][RBW * G::ROWB];
+  int offs[NSTG][RBW];
+  uint64_t bar[NSTG];
 };
 
 template <int WPC = kWarpsPerCta>
@@ -159,8 +163,7 @@ __device__ __forceinline__ void warp_tile(int nJ, int nK, int& J, int& K) {
 template <typename WS>
 __device__ __forceinline__ void warp_stage_init(WS& ws, int lane) {
   if (lane == 0) {
-    mbar_init(&ws.bar[0], 1);
-    mbar_init(&ws.bar[1], 1);
+    for (int i = 0; i < WS::NSTG; ++i) mbar_init(&ws.bar[i], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -481,14 +484,24 @@ __global__ void sat_apply_carry_kernel(Acc* __restrict__ colp, const Acc* __rest
 
 // ---------------------------------------------------------------------------
 // phase 3
+#ifndef SSB_SCAN_STHINT
+#define SSB_SCAN_STHINT 0
+#endif
 template <typename Acc, int E>
 __device__ __forceinline__ void store_lane_cols(Acc* __restrict__ dst, const Acc (&v)[E], int64_t col, int64_t PC) {
   if (col + E <= PC) {
+#if SSB_SCAN_STHINT
+    const uint64_t pol = SSB_SCAN_STHINT == 1 ? policy_evict_first() : policy_evict_last();
+#endif
 #pragma unroll
     for (int k = 0; k < E; k += 4) {
       U64x4 q;
       memcpy(&q, &v[k], 32);
+#if SSB_SCAN_STHINT
+      st256_hint(dst + k, q, pol);
+#else
       st256(dst + k, q);
+#endif
     }
   } else {
 #pragma unroll
@@ -509,8 +522,8 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
   using LocSq = typename Tr::LocSq;
   using Acc = typename Tr::Acc;
   using G = Geo<InT>;
-  using WS = WarpStage<InT>;
-  constexpr int TW = G::TW, E = G::E, RB = WS::RBW;
+  using WS = WarpStage<InT, 0, SSB_SCAN_STAGES>;
+  constexpr int TW = G::TW, E = G::E, RB = WS::RBW, NSTG = WS::NSTG;
   static_assert(E % 4 == 0, "256-bit stores");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WS* stages = reinterpret_cast<WS*>(smem_raw);
@@ -526,7 +539,14 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
   const int64_t cbase = j0 + lane * E;  // table column of the lane's first element
   const int64_t c0 = cbase - 1;         // matching image column
   warp_stage_init(ws, lane);
-  stage_issue<InT, RB>(ws.buf[0], ws.offs[0], &ws.bar[0], in, R, C, in_ld, k0, (int)min64(RB, k1 - k0), j0, lane);
+#pragma unroll
+  for (int pb = 0; pb < NSTG - 1; ++pb) {
+    if (pb < nblk) {
+      const int64_t rp = k0 + (int64_t)pb * RB;
+      stage_issue<InT, RB>(ws.buf[pb], ws.offs[pb], &ws.bar[pb], in, R, C, in_ld, rp, (int)min64(RB, k1 - rp), j0,
+                           lane);
+    }
+  }
 
   Acc acc[E], accq[E];
 #pragma unroll
@@ -537,20 +557,21 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
   const bool writes_plain = sat != nullptr;
 
   for (int b = 0; b < nblk; ++b) {
-    const int s = b & 1;
+    const int s = b % NSTG;
     const int64_t r0 = k0 + (int64_t)b * RB;
     const int nr = (int)min64(RB, k1 - r0);
-    if (b + 1 < nblk) {
-      const int64_t rn = r0 + RB;
-      stage_issue<InT, RB>(ws.buf[s ^ 1], ws.offs[s ^ 1], &ws.bar[s ^ 1], in, R, C, in_ld, rn,
-                           (int)min64(RB, k1 - rn), j0, lane);
+    if (b + NSTG - 1 < nblk) {  // refill the stage consumed in iteration b - 1
+      const int sn = (b + NSTG - 1) % NSTG;
+      const int64_t rn = r0 + (int64_t)(NSTG - 1) * RB;
+      stage_issue<InT, RB>(ws.buf[sn], ws.offs[sn], &ws.bar[sn], in, R, C, in_ld, rn, (int)min64(RB, k1 - rn), j0,
+                           lane);
     }
     Acc rlv = Acc(0), rlqv = Acc(0);  // lane r: left carry of row r
     if (lane < nr) {
       rlv = rl[(r0 + lane) * nJ + J];
       if constexpr (SQ) rlqv = rl_sq[(r0 + lane) * nJ + J];
     }
-    mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
+    mbar_wait(&ws.bar[s], (uint32_t)((b / NSTG) & 1));
     for (int r = 0; r < nr; ++r) {
       uint32_t o[Pack<InT>::NW];
       lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
@@ -1121,7 +1142,10 @@ inline SatPlan make_sat_plan(int dtype, int64_t R, int64_t C, bool sq) {
   p.PR = R + 1; p.PC = C + 1;
   p.nJ = (int)((p.PC + p.TW - 1) / p.TW);
   const int RB = 8;  // segment height is a multiple of every kernel's row block
-  const int64_t target_tiles = 64LL * kNumSMs;  // warp tiles: ~4 waves of 16 warps per SM
+#ifndef SSB_TILES_PER_SM
+#define SSB_TILES_PER_SM 64
+#endif
+  const int64_t target_tiles = (int64_t)SSB_TILES_PER_SM * kNumSMs;  // warp tiles: ~4 waves of 16 warps per SM
   int64_t wantK = (target_tiles + p.nJ - 1) / p.nJ;
   int64_t SR = (p.PR + wantK - 1) / wantK;
   SR = ((SR + RB - 1) / RB) * RB;
@@ -1211,7 +1235,7 @@ cudaError_t launch_sat_finish_t(const void* in, int64_t R, int64_t C, int64_t in
   if (carry) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp, reinterpret_cast<const Acc*>(carry), p.nK, p.PC); note_launch(1); }
   if (SQ && carry_sq) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp_sq, reinterpret_cast<const Acc*>(carry_sq), p.nK, p.PC); note_launch(1); }
   const int tb = (int)(((int64_t)p.nJ * p.nK + kWarpsPerCta - 1) / kWarpsPerCta);
-  const int smem = (int)(sizeof(WarpStage<InT>) * kWarpsPerCta);
+  const int smem = (int)(sizeof(WarpStage<InT, 0, SSB_SCAN_STAGES>) * kWarpsPerCta);
   cudaError_t e = cudaFuncSetAttribute(sat_scan_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   sat_scan_kernel<InT, SQ><<<tb, kThreads, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
