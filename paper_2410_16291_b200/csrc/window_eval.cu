@@ -269,10 +269,10 @@ template <> struct FinK<double> {
 // even number of elements covering [j0, j0 + CW + w) (reads reach index CW - 1 + w)
 __host__ __device__ __forceinline__ int64_t seg_need(int64_t cw, int64_t w) { return (cw + w + 1) & ~int64_t(1); }
 
-template <typename Acc, bool SQ, int U, bool MULTI>
+template <typename Acc, bool SQ, int U, bool MULTI, bool HINTS>
 __global__ void __launch_bounds__(kThreads + 32)
 window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, const __grid_constant__ MultiEval g,
-                       unsigned long long* __restrict__ ticket, int NS, int batch, int hints) {
+                       unsigned long long* __restrict__ ticket, int NS, int batch) {
   constexpr int NT = SQ ? 2 : 1;
   constexpr int kTmaCW = kThreads * U;  // output columns per item
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -325,7 +325,8 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
       ++dp;
       dcpp = ((int64_t)dp == g.n_panels - 1) ? cppl : cppf;
     };
-    const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+    uint64_t pol_keep = 0, pol_drop = 0;
+    if constexpr (HINTS) { pol_keep = policy_evict_last(); pol_drop = policy_evict_first(); }
     uint32_t s = 0, phase = 0;
     for (int64_t m = 0;; ++m) {
       if (m >= NS) mbar_wait(&empty[s], phase ^ 1u);
@@ -369,7 +370,7 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
         fence_proxy_async();
         mbar_arrive_expect_tx(&full[s], (bytes + bb) * NT);
         Acc* b = buf + (int64_t)s * stage_stride;
-        if (hints) {
+        if constexpr (HINTS) {
           // bottom rows come back as top rows w rows later: keep them in L2;
           // a top row of the largest window is read for the last time
           bulk_g2s_hint(b, sat + rb * ld + j0, bb, &full[s], pol_keep);
@@ -383,7 +384,7 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
           const int64_t len = seg_need(kTmaCW, g.w[k]);
           const uint32_t tb = (uint32_t)((len < avail ? len : avail) * 8);
           const int64_t top = (rb - g.w[k]) * ld + j0;
-          if (hints) {
+          if constexpr (HINTS) {
             const uint64_t pol = g.w[k] == g.wmax ? pol_drop : pol_keep;
             bulk_g2s_hint(b + g.off[k], sat + top, tb, &full[s], pol);
             if constexpr (SQ) bulk_g2s_hint(b + g.stage_elems + g.off[k], sq + top, tb, &full[s], pol);
@@ -405,20 +406,25 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
       const int64_t j0 = meta_j0[s];
       const int mask = meta_mask[s];
       const Acc* B = buf + (int64_t)s * stage_stride;
-#pragma unroll 1
-      for (int k = 0; k < nwin; ++k) {
-        if (!((mask >> k) & 1)) continue;
+      // bottom-left corners are shared by every window
+      Acc bl[U], blq[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bl[u] = B[tid + kThreads * u];
+        if constexpr (SQ) blq[u] = B[g.stage_elems + tid + kThreads * u];
+      }
+      auto window = [&](int k) {
         const int w = (int)g.w[k];
         const Acc* T = B + g.off[k];
         Acc sv[U], qv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int jj = tid + kThreads * u;
-          sv[u] = corner4<Acc>(B[jj + w], T[jj + w], B[jj], T[jj]);
+          sv[u] = corner4<Acc>(B[jj + w], T[jj + w], bl[u], T[jj]);
           if constexpr (SQ) {
             const Acc* BQ = B + g.stage_elems;
             const Acc* TQ = T + g.stage_elems;
-            qv[u] = corner4<Acc>(BQ[jj + w], TQ[jj + w], BQ[jj], TQ[jj]);
+            qv[u] = corner4<Acc>(BQ[jj + w], TQ[jj + w], blq[u], TQ[jj]);
           }
         }
         const WinOut& o = g.o[k];
@@ -434,6 +440,15 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
           if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(sv[u]));
           if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(sv[u], qv[u]));
         }
+      };
+      if constexpr (MULTI) {
+        // a rolled loop: the 8-slot unrolled form ran slower (instruction
+        // cache pressure) despite fewer instructions
+#pragma unroll 1
+        for (int k = 0; k < nwin; ++k)
+          if ((mask >> k) & 1) window(k);
+      } else {
+        window(0);
       }
     }
     __syncwarp();
@@ -489,7 +504,10 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   m.cpp = m.pw / kTmaCW;
   m.cpl = (out_c_max - (m.n_panels - 1) * m.pw + kTmaCW - 1) / kTmaCW;
   const bool multi = m.nwin > 1;
-  auto kfn = multi ? window_eval_tma_kernel<Acc, SQ, U, true> : window_eval_tma_kernel<Acc, SQ, U, false>;
+  const char* env_h = getenv("SSB_EVAL_TMA_HINTS");  // tuning: L2 policies on the table row copies
+  const bool hints = env_h ? atoi(env_h) != 0 : !multi;
+  auto kfn = multi ? (hints ? window_eval_tma_kernel<Acc, SQ, U, true, true> : window_eval_tma_kernel<Acc, SQ, U, true, false>)
+                   : (hints ? window_eval_tma_kernel<Acc, SQ, U, false, true> : window_eval_tma_kernel<Acc, SQ, U, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -505,10 +523,8 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   unsigned long long* ticket = tickets + (slot.fetch_add(1) % 256);
   e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  const char* env_h = getenv("SSB_EVAL_TMA_HINTS");  // tuning: L2 policies on the table row copies
-  const int hints = env_h ? atoi(env_h) : (m.nwin == 1 ? 1 : 0);
   kfn<<<blocks, kThreads + 32, smem, st>>>(reinterpret_cast<const Acc*>(sat), reinterpret_cast<const Acc*>(sat_sq),
-                                           m, ticket, NS, batch, hints);
+                                           m, ticket, NS, batch);
   used = true;
   return cudaGetLastError();
 }
