@@ -118,12 +118,19 @@ def emit(obj: dict) -> None:
     print(json.dumps(obj), flush=True)
 
 
+_BANDS: dict = {}
+
+
 def cpu_port_band(out_rows: int, threads: int = 0):
-    """Reference algorithm (oracle port) on output rows [0, out_rows) of C5; returns (seconds, pixels)."""
+    """Reference algorithm (oracle port) on output rows [0, out_rows) of C5; returns (seconds, pixels).
+
+    The band is generated once per size (untimed) and reused across steps."""
     from oracle import satsweep_oracle as oracle
     from paper_2410_16291_b200 import synthetic
 
-    band = synthetic.c5(0, out_rows + W - 1)
+    if out_rows not in _BANDS:
+        _BANDS[out_rows] = synthetic.c5(0, out_rows + W - 1)
+    band = _BANDS[out_rows]
     t0 = time.perf_counter()
     res = oracle.swa_threaded(band, W, "sum", 1, threads or (os.cpu_count() or 1))
     dt = time.perf_counter() - t0
@@ -165,7 +172,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--ref-rows", type=int, default=4096, help="output rows per reference/CPU step")
+    ap.add_argument("--ref-rows", type=int, default=16384, help="output rows per reference/CPU step")
     ap.add_argument("--cpu-rows", type=int, default=16384, help="output rows of the cpu_baseline sample")
     ap.add_argument("--cpu-reps", type=int, default=8, help="repetitions of the cpu_baseline sample (~10-30 s of CPU work)")
     ap.add_argument("--no-e2e", action="store_true")
