@@ -40,6 +40,9 @@
 #ifndef SSB_SCAN_STAGES
 #define SSB_SCAN_STAGES 2
 #endif
+#ifndef SSB_SCAN_MINB_SQ
+#define SSB_SCAN_MINB_SQ 2
+#endif
 
 namespace ssb {
 
@@ -94,6 +97,17 @@ __device__ __forceinline__ void lane_words(const unsigned char* stage, const int
 }
 
 // sum of the lane's elements in Loc / of their squares in LocSq
+// pairwise (tree) sum of E values: log2(E) dependent adds instead of E
+template <int N, typename T>
+__device__ __forceinline__ T tree_sum(T (&v)[N]) {
+#pragma unroll
+  for (int h = N / 2; h >= 1; h /= 2) {
+#pragma unroll
+    for (int k = 0; k < h; ++k) v[k] = add(v[k], v[k + h]);
+  }
+  return v[0];
+}
+
 template <typename InT>
 __device__ __forceinline__ typename Elem<InT>::Loc lane_total(const uint32_t* o) {
   using Loc = typename Elem<InT>::Loc;
@@ -101,6 +115,11 @@ __device__ __forceinline__ typename Elem<InT>::Loc lane_total(const uint32_t* o)
   if constexpr (sizeof(InT) == 1) {
 #pragma unroll
     for (int i = 0; i < Pack<InT>::NW; ++i) t = __dp4a(o[i], 0x01010101u, t);
+  } else if constexpr (Elem<InT>::kFloat) {
+    Loc v[Geo<InT>::E];
+#pragma unroll
+    for (int k = 0; k < Geo<InT>::E; ++k) v[k] = conv<Loc>(elem<InT>(o, k));
+    t = tree_sum(v);
   } else {
 #pragma unroll
     for (int k = 0; k < Geo<InT>::E; ++k) t = add(t, conv<Loc>(elem<InT>(o, k)));
@@ -114,6 +133,11 @@ __device__ __forceinline__ typename Elem<InT>::LocSq lane_total_sq(const uint32_
   if constexpr (sizeof(InT) == 1) {
 #pragma unroll
     for (int i = 0; i < Pack<InT>::NW; ++i) t = __dp4a(o[i], o[i], t);
+  } else if constexpr (Elem<InT>::kFloat) {
+    LocSq v[Geo<InT>::E];
+#pragma unroll
+    for (int k = 0; k < Geo<InT>::E; ++k) v[k] = convsq<LocSq>(elem<InT>(o, k));
+    t = tree_sum(v);
   } else {
 #pragma unroll
     for (int k = 0; k < Geo<InT>::E; ++k) t = add(t, convsq<LocSq>(elem<InT>(o, k)));
@@ -218,8 +242,11 @@ __device__ __forceinline__ T warp_reduce_scatter(T (&v)[N], int lane) {
 #ifndef SSB_REDUCE_MINB
 #define SSB_REDUCE_MINB 3
 #endif
+#ifndef SSB_REDUCE_MINB_SQ
+#define SSB_REDUCE_MINB_SQ 2
+#endif
 template <typename InT, bool SQ, int RBR, int WPC>
-__global__ void __launch_bounds__(32 * WPC, SQ ? 1 : SSB_REDUCE_MINB)
+__global__ void __launch_bounds__(32 * WPC, SQ ? SSB_REDUCE_MINB_SQ : SSB_REDUCE_MINB)
 sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                   typename Elem<InT>::Acc* __restrict__ rowtot, typename Elem<InT>::Acc* __restrict__ rowtot_sq,
                   typename Elem<InT>::Acc* __restrict__ colp, typename Elem<InT>::Acc* __restrict__ colp_sq,
@@ -511,7 +538,7 @@ __device__ __forceinline__ void store_lane_cols(Acc* __restrict__ dst, const Acc
 }
 
 template <typename InT, bool SQ>
-__global__ void __launch_bounds__(kThreads, SQ ? 2 : SSB_SCAN_MINB)
+__global__ void __launch_bounds__(kThreads, SQ ? SSB_SCAN_MINB_SQ : SSB_SCAN_MINB)
 sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                 typename Elem<InT>::Acc* __restrict__ sat, typename Elem<InT>::Acc* __restrict__ sat_sq, int64_t sat_ld,
                 const typename Elem<InT>::Acc* __restrict__ rl, const typename Elem<InT>::Acc* __restrict__ rl_sq,
