@@ -476,28 +476,37 @@ sat_segsum_kernel(const Acc* __restrict__ rl, Acc* __restrict__ srl, int nJ, int
 // phase 2b: table row above every segment (without any band carry), in place
 // over the column prefixes.  The final running value is the image's last table
 // row -- the band column totals used by row-band shards.
+// 32 columns x kTopChunks segment chunks per CTA: each thread sums its chunk,
+// an exclusive scan over the chunks gives its offset, then it rewrites its
+// chunk -- kTopChunks-way parallel down the segments instead of one serial walk.
+constexpr int kTopChunks = 8;
 template <typename Acc>
-__global__ void sat_topcarry_kernel(Acc* __restrict__ colp, const Acc* __restrict__ srl, Acc* __restrict__ totals,
-                                    int nK, int nJ, int64_t PC, int TW) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= PC) return;
-  const int J = (int)(j / TW);
-  constexpr int B = 8;
-  Acc run = Acc(0);
-  for (int K0 = 0; K0 < nK; K0 += B) {
-    Acc v[B], sr[B];
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      v[k] = (K0 + k < nK) ? colp[(int64_t)(K0 + k) * PC + j] : Acc(0);
-      sr[k] = (K0 + k < nK) ? srl[(int64_t)(K0 + k) * nJ + J] : Acc(0);
-    }
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      if (K0 + k < nK) colp[(int64_t)(K0 + k) * PC + j] = run;
-      run = add(run, add(v[k], sr[k]));
-    }
+__global__ void __launch_bounds__(32 * kTopChunks)
+sat_topcarry_kernel(Acc* __restrict__ colp, const Acc* __restrict__ srl, Acc* __restrict__ totals, int nK, int nJ,
+                    int64_t PC, int TW) {
+  __shared__ Acc part[kTopChunks][32];
+  const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + c;
+  const bool live = j < PC;
+  const int J = live ? (int)(j / TW) : 0;
+  const int ch = (nK + kTopChunks - 1) / kTopChunks;
+  const int ka = q * ch, kb = min(nK, ka + ch);
+  Acc sum = Acc(0);
+  if (live) {
+    for (int K = ka; K < kb; ++K) sum = add(sum, add(colp[(int64_t)K * PC + j], srl[(int64_t)K * nJ + J]));
   }
-  if (totals) totals[j] = run;
+  part[q][c] = sum;
+  __syncthreads();
+  Acc run = Acc(0);
+  for (int p = 0; p < q; ++p) run = add(run, part[p][c]);
+  if (live) {
+    for (int K = ka; K < kb; ++K) {
+      const Acc v = add(colp[(int64_t)K * PC + j], srl[(int64_t)K * nJ + J]);
+      colp[(int64_t)K * PC + j] = run;
+      run = add(run, v);
+    }
+    if (totals && q == kTopChunks - 1) totals[j] = run;
+  }
 }
 
 // adds a carry row to every segment's top row (row-band shards)
@@ -1241,9 +1250,9 @@ cudaError_t launch_sat_prepare_t(const void* in, int64_t R, int64_t C, int64_t i
   const dim3 sgrid(p.nK, (p.nJ + 31) / 32);
   sat_segsum_kernel<Acc><<<sgrid, kThreads, 0, st>>>(rowtot, srl, p.nJ, p.PR, p.SR);
   if (SQ) sat_segsum_kernel<Acc><<<sgrid, kThreads, 0, st>>>(rowtot_sq, srl_sq, p.nJ, p.PR, p.SR);
-  const int nb_cols = (int)((p.PC + kThreads - 1) / kThreads);
-  sat_topcarry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp, srl, reinterpret_cast<Acc*>(totals), p.nK, p.nJ, p.PC, p.TW);
-  if (SQ) sat_topcarry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp_sq, srl_sq, reinterpret_cast<Acc*>(totals_sq), p.nK, p.nJ, p.PC, p.TW);
+  const int nb_top = (int)((p.PC + 31) / 32);
+  sat_topcarry_kernel<Acc><<<nb_top, 32 * kTopChunks, 0, st>>>(colp, srl, reinterpret_cast<Acc*>(totals), p.nK, p.nJ, p.PC, p.TW);
+  if (SQ) sat_topcarry_kernel<Acc><<<nb_top, 32 * kTopChunks, 0, st>>>(colp_sq, srl_sq, reinterpret_cast<Acc*>(totals_sq), p.nK, p.nJ, p.PC, p.TW);
   note_launch(SQ ? 7 : 4);
   return cudaGetLastError();
 }

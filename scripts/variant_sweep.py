@@ -20,7 +20,8 @@ def main():
                 "build_ext.build(defines=%r, lib=__import__('pathlib').Path(%r))" % (str(REPO), defines, str(lib)))
         subprocess.run([sys.executable, "-c", code], check=True)
         env = dict(os.environ, SSB_LIB=str(lib))
-        out = subprocess.run([sys.executable, str(REPO / script)], env=env, capture_output=True, text=True)
+        parts = script.split()
+        out = subprocess.run([sys.executable, str(REPO / parts[0]), *parts[1:]], env=env, capture_output=True, text=True)
         for line in (out.stdout + out.stderr).strip().splitlines()[-3:]:
             print(f"[{v}] {line}", flush=True)
 
