@@ -207,7 +207,10 @@ def main() -> None:
     t_gen = time.perf_counter()
     host_band = synthetic.c5(a_own, b_own) if rows == ROWS else synthetic.bernoulli_rows(5, rows, COLS, 0.01, a_own, b_own)
     gen_s = time.perf_counter() - t_gen
-    x_own = _device.to_device(host_band, dev)
+    # zero-copy halo layout: the band lives at the head of a buffer with room
+    # for its halo, which NCCL receives in place each step (no concatenation)
+    storage, x_own = shard.band_storage(rows, COLS, W, 1, torch.uint8, dev)
+    x_own.copy_(torch.from_numpy(host_band))
     del host_band
     need = shard.window_needed_rows(rows, W, 1, world)[rank]
     nr = need[1] - need[0]
@@ -225,7 +228,7 @@ def main() -> None:
     def get_x():
         if world == 1:
             return x_own
-        return shard.halo_exchange(x_own, rows, W, 1, group)
+        return shard.halo_exchange(x_own, rows, W, 1, group, storage=storage)
 
     ev = {k: [] for k in ("build", "eval")}
 

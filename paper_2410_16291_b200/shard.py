@@ -94,11 +94,29 @@ def table_input_bands(rows: int, n: int) -> list[tuple[int, int]]:
 
 
 # ----------------------------------------------------------------------------- exchange
-def halo_exchange(band, rows: int, w: int, stride: int, group=None):
+def band_storage(rows: int, cols: int, w: int, stride: int, dtype, device=None, group=None):
+    """Zero-copy layout for the window path: a tensor with room for this rank's
+    band plus its halo, and the view holding the owned rows.  Fill the view,
+    then pass both to ``halo_exchange(view, ..., storage=storage)``: the halo
+    rows are received straight into the tail, so no per-step concatenation
+    (a full read + write of the band) is needed."""
+    import torch
+
+    rank, n = world(group)
+    a_own, b_own = window_input_bands(rows, w, stride, n)[rank]
+    a_need, b_need = window_needed_rows(rows, w, stride, n)[rank]
+    lo, hi = min(a_own, a_need) if b_need > a_need else a_own, max(b_own, b_need)
+    storage = torch.empty((hi - lo, cols), dtype=dtype, device=device)
+    return storage, storage[a_own - lo:b_own - lo]
+
+
+def halo_exchange(band, rows: int, w: int, stride: int, group=None, storage=None):
     """Return this rank's band extended by the halo rows it needs (P2P send/recv).
 
     ``band`` is a 2-D tensor holding exactly the rows ``window_input_bands``
-    assigns to this rank."""
+    assigns to this rank.  With ``storage`` (from ``band_storage``, ``band``
+    being its owned-rows view) the halo is received in place and the needed
+    rows are returned as a view -- no copy of the band."""
     import torch
 
     dist = _dist()
@@ -110,6 +128,11 @@ def halo_exchange(band, rows: int, w: int, stride: int, group=None):
     a_need, b_need = need[rank]
     if n == 1 or b_need <= a_need:
         return band[max(0, a_need - a_own):max(0, b_need - a_own)]
+    base = None  # global row held by storage[0]
+    if storage is not None:
+        base = min(a_own, a_need)
+        assert storage.shape[0] >= max(b_own, b_need) - base
+        assert band.data_ptr() == storage[a_own - base:].data_ptr(), "band must be the owned-rows view of storage"
     ops, recv = [], []
     # what I receive: rows of [a_need, b_need) owned by other ranks
     for src in range(n):
@@ -118,7 +141,10 @@ def halo_exchange(band, rows: int, w: int, stride: int, group=None):
         a, b = owned[src]
         lo, hi = max(a, a_need), min(b, b_need)
         if hi > lo:
-            buf = torch.empty((hi - lo,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
+            if base is not None:
+                buf = storage[lo - base:hi - base]
+            else:
+                buf = torch.empty((hi - lo,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
             recv.append((lo, buf))
             ops.append(dist.P2POp(dist.irecv, buf, src, group))
     # what I send: my rows inside other ranks' needs
@@ -132,6 +158,8 @@ def halo_exchange(band, rows: int, w: int, stride: int, group=None):
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    if base is not None:
+        return storage[a_need - base:b_need - base]
     pieces = []
     lo_own, hi_own = max(a_own, a_need), min(b_own, b_need)
     if hi_own > lo_own:
@@ -226,11 +254,13 @@ class ShardedResult:
 
 
 def swa_sharded(band, rows: int, cols: int, kind: ElemKind, w: int, stats=(StatKind.SUM,), stride: int = 1,
-                pipeline: str = "auto", backend=None, group=None) -> ShardedResult:
-    """Window statistics of a row-sharded image; outputs stay sharded on the ranks."""
+                pipeline: str = "auto", backend=None, group=None, storage=None) -> ShardedResult:
+    """Window statistics of a row-sharded image; outputs stay sharded on the ranks.
+
+    ``storage``: see ``band_storage`` (zero-copy halo)."""
     rank, n = world(group)
     backend = backend or CudaBackend()
-    x = halo_exchange(band, rows, w, stride, group)
+    x = halo_exchange(band, rows, w, stride, group, storage=storage)
     out_r = (rows - w) // stride + 1
     lo, hi = output_partition(out_r, n)[rank]
     if hi <= lo:

@@ -89,6 +89,14 @@ def _worker(rank, world, port, img, w, stride, q):
         res = shard.swa_sharded(torch.from_numpy(img[a:b].copy()), rows, cols, kind, w,
                                 (StatKind.SUM, StatKind.MEAN), stride, backend=NumpyBackend())
         win = {k.value: v.numpy() for k, v in res.values.items()}
+        # zero-copy layout: halo received in place into the band's storage
+        storage, view = shard.band_storage(rows, cols, w, stride, torch.from_numpy(img).dtype)
+        a, b = shard.window_input_bands(rows, w, stride, world)[rank]
+        view.copy_(torch.from_numpy(img[a:b]))
+        res2 = shard.swa_sharded(view, rows, cols, kind, w, (StatKind.SUM, StatKind.MEAN), stride,
+                                 backend=NumpyBackend(), storage=storage)
+        for k, v in res2.values.items():
+            assert np.array_equal(v.numpy(), win[k.value]), k
         a, b = shard.table_input_bands(rows, world)[rank]
         tab = shard.build_sat_sharded(torch.from_numpy(img[a:b].copy()), rows, cols, kind, backend=NumpyBackend())
         q.put((rank, res.rows, win, tab.rows, tab.values["table"].numpy()))
