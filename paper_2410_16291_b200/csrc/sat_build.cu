@@ -123,6 +123,12 @@ sat_reduce_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_l
                            (int)min64(RB, k1 - rn), j0, lane);
     }
     mbar_wait(&ws.bar[s], (uint32_t)((b >> 1) & 1));
+#ifdef SSB_REDUCE_LOADONLY
+    // tuning probe: staging only (measures the read pattern's bandwidth)
+    if (lane == 0) rowtot[r0 * nJ + J] += ws.buf[s][16];
+    __syncwarp();
+    continue;
+#endif
     Loc part[RB];      // lane partial of each staged row
     LocSq part_sq[RB];
     // interior blocks (all RB rows are image rows) on interior lanes (all E
