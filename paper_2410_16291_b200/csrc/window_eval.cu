@@ -476,7 +476,9 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   const char* env_b = getenv("SSB_EVAL_BATCH");
   const int batch = env_b ? atoi(env_b) : 4;
   const char* env_ns = getenv("SSB_EVAL_STAGES");
-  int NS = env_ns ? atoi(env_ns) : 3;
+  // multi-window stages are large (a top segment per window): 2 stages keep
+  // 3 CTAs per SM resident (C3 sweep 9.2 -> 8.5 ms); single window: 3 stages
+  int NS = env_ns ? atoi(env_ns) : (m.nwin > 1 ? 2 : 3);
   if (NS < 2) NS = 2;
   if (NS > kTmaMaxNS) NS = kTmaMaxNS;
   // stage layout: bottom segment (covers the widest window), then one top
@@ -535,6 +537,7 @@ cudaError_t launch_tma_multi(const void* sat, const void* sat_sq, const MultiEva
   // two CTAs per SM resident (tuning: SSB_EVAL_U=2|4)
   const char* env_u = getenv("SSB_EVAL_U");
   const int u = env_u ? atoi(env_u) : (m.nwin > 2 ? 2 : 4);
+  if (u == 1) return launch_tma_multi_u<Acc, SQ, 1>(sat, sat_sq, m, st, used);
   if (u == 2) return launch_tma_multi_u<Acc, SQ, 2>(sat, sat_sq, m, st, used);
   return launch_tma_multi_u<Acc, SQ, 4>(sat, sat_sq, m, st, used);
 }
