@@ -345,29 +345,47 @@ def main() -> None:
     except Exception as exc:  # pragma: no cover - reporting only
         result["fused"] = {"error": str(exc)}
 
-    # ---- e2e through the public API with pinned host buffers (rank-local band)
-    if not args.no_e2e and world == 1:
+    # ---- e2e through the public API with pinned host buffers: every rank runs
+    # swa on its own input rows (band + halo) and reads back its output band;
+    # the step time is the max over ranks
+    if not args.no_e2e:
         try:
+            x_need = get_x()
             del sat, ws
             torch.cuda.empty_cache()
-            host_in = torch.empty((rows, COLS), dtype=torch.uint8, pin_memory=True)
-            _copy_chunks(host_in, x_own)
-            host_out = torch.empty((rows - W + 1, out_c), dtype=torch.int64, pin_memory=True)
+            host_in = torch.empty((nr, COLS), dtype=torch.uint8, pin_memory=True)
+            _copy_chunks(host_in, x_need)
+            host_out = torch.empty((max(n_out, 1), out_c), dtype=torch.int64, pin_memory=True)
             import paper_2410_16291_b200 as sb
 
             hin = host_in.numpy()
-            hout = host_out.numpy().view(np.uint64)
-            sb.swa(hin, W, "sum", pipeline="table", out=hout)  # warm-up
+            hout = host_out.numpy().view(np.uint64)[:n_out]
+
+            def e2e_step():
+                if n_out > 0:
+                    sb.swa(hin, W, "sum", pipeline="table", out=hout)
+
+            e2e_step()  # warm-up
             times = []
             for _ in range(args.e2e_steps):
+                barrier()
                 t0 = time.perf_counter()
-                sb.swa(hin, W, "sum", pipeline="table", out=hout)
+                e2e_step()
                 times.append(time.perf_counter() - t0)
             te = sum(times) / len(times)
-            result["e2e"] = {"value": rows * COLS / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": rows * COLS,
-                             "d2h_bytes_per_step": (rows - W + 1) * out_c * 8, "s_per_step": te,
+            h2d, d2h = nr * COLS, n_out * out_c * 8
+            if world > 1:
+                import torch.distributed as dist
+
+                agg = torch.tensor([te, float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+                mx = agg[:1].clone()
+                dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+                dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+                te, h2d, d2h = float(mx.item()), int(agg[1].item()), int(agg[2].item())
+            result["e2e"] = {"value": rows * COLS / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                             "d2h_bytes_per_step": d2h, "s_per_step": te,
                              "api": "paper_2410_16291_b200.swa(numpy pinned, 256, 'sum', pipeline='table', out=pinned)"
-                                    " -> ssb_swa_host"}
+                                    " -> ssb_swa_host, per rank on its band + halo; max over ranks"}
         except Exception as exc:  # pragma: no cover
             result["e2e"] = {"error": str(exc)}
 
