@@ -361,8 +361,12 @@ __global__ void sat_apply_carry_kernel(Acc* __restrict__ colp, const Acc* __rest
 
 // ---------------------------------------------------------------------------
 // phase 3
+#ifndef SSB_SCAN_WPC
+#define SSB_SCAN_WPC 8
+#endif
+constexpr int kScanWarps = SSB_SCAN_WPC;
 template <typename InT, bool SQ>
-__global__ void __launch_bounds__(kThreads, SQ ? SSB_SCAN_MINB_SQ : SSB_SCAN_MINB)
+__global__ void __launch_bounds__(32 * kScanWarps, SQ ? SSB_SCAN_MINB_SQ : SSB_SCAN_MINB)
 sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                 typename Elem<InT>::Acc* __restrict__ sat, typename Elem<InT>::Acc* __restrict__ sat_sq, int64_t sat_ld,
                 const typename Elem<InT>::Acc* __restrict__ rl, const typename Elem<InT>::Acc* __restrict__ rl_sq,
@@ -381,7 +385,7 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
   const int lane = threadIdx.x & 31;
   WS& ws = stages[threadIdx.x >> 5];
   int J, K;
-  warp_tile(nJ, nK, J, K);
+  warp_tile<kScanWarps>(nJ, nK, J, K);
   if (K < 0) return;
   const int64_t PR = R + 1, PC = C + 1;
   const int64_t j0 = (int64_t)J * TW, k0 = (int64_t)K * SR;
@@ -423,6 +427,16 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
       if constexpr (SQ) rlqv = rl_sq[(r0 + lane) * nJ + J];
     }
     mbar_wait(&ws.bar[s], (uint32_t)((b / NSTG) & 1));
+#ifdef SSB_SCAN_STOREONLY
+    // tuning probe: the table stores without the row arithmetic
+    for (int r = 0; r < nr; ++r) {
+#pragma unroll
+      for (int k = 0; k < E; ++k) acc[k] = add(acc[k], (Acc)rlv);
+      if (writes_plain) store_lane_cols<Acc, E>(sat + (r0 + r) * sat_ld + cbase, acc, cbase, PC);
+    }
+    __syncwarp();
+    continue;
+#endif
     for (int r = 0; r < nr; ++r) {
       uint32_t o[Pack<InT>::NW];
       lane_words<InT>(ws.buf[s], ws.offs[s], r, c0, C, o);
@@ -478,7 +492,10 @@ inline SatPlan make_sat_plan(int dtype, int64_t R, int64_t C, bool sq) {
   int64_t wantK = (target_tiles + p.nJ - 1) / p.nJ;
   int64_t SR = (p.PR + wantK - 1) / wantK;
   SR = ((SR + RB - 1) / RB) * RB;
-  if (SR > 1024) SR = 1024;
+#ifndef SSB_SR_CAP
+#define SSB_SR_CAP 512
+#endif
+  if (SR > SSB_SR_CAP) SR = SSB_SR_CAP;
   if (SR < RB) SR = RB;
   p.SR = SR;
   p.nK = (int)((p.PR + SR - 1) / SR);
@@ -570,11 +587,11 @@ cudaError_t launch_sat_finish_t(const void* in, int64_t R, int64_t C, int64_t in
   const int nb_cols = (int)((p.PC + kThreads - 1) / kThreads);
   if (carry) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp, reinterpret_cast<const Acc*>(carry), p.nK, p.PC); note_launch(1); }
   if (SQ && carry_sq) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp_sq, reinterpret_cast<const Acc*>(carry_sq), p.nK, p.PC); note_launch(1); }
-  const int tb = (int)(((int64_t)p.nJ * p.nK + kWarpsPerCta - 1) / kWarpsPerCta);
-  const int smem = (int)(sizeof(WarpStage<InT, 0, SSB_SCAN_STAGES>) * kWarpsPerCta);
+  const int tb = (int)(((int64_t)p.nJ * p.nK + kScanWarps - 1) / kScanWarps);
+  const int smem = (int)(sizeof(WarpStage<InT, 0, SSB_SCAN_STAGES>) * kScanWarps);
   cudaError_t e = cudaFuncSetAttribute(sat_scan_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  sat_scan_kernel<InT, SQ><<<tb, kThreads, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
+  sat_scan_kernel<InT, SQ><<<tb, 32 * kScanWarps, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
                                                     reinterpret_cast<Acc*>(sat), reinterpret_cast<Acc*>(sat_sq),
                                                     sat_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ, p.nK);
   note_launch(1);
