@@ -144,6 +144,33 @@ def eval_tables(sat, sq, ld: int, kind: ElemKind, rows: int, cols: int, w: int, 
     return outs
 
 
+def sweep_supported(kind: ElemKind, w: int, stride: int, stats) -> bool:
+    """Whether ssb_sat_build_swa (table + window sums in one pass) takes this request."""
+    return stride == 1 and bool(_lib.load().ssb_sat_swa_supported(kind.abi_code, w, stat_mask(stats)))
+
+
+def table_and_sweep(x, kind: ElemKind, rows: int, cols: int, w: int, stats, device, *, outs=None,
+                    scratch: bool = False):
+    """Integral image AND its stride-1 window stats in one pass (ssb_sat_build_swa).
+
+    Same table as build_tables and same outputs as eval_tables on it, but the
+    table is never read back.  Returns (sat, sat_ld, outs)."""
+    lib = _lib.load()
+    ld = sat_ld_for(cols)
+    tbytes = (rows + 1) * ld * 8
+    sat = (_table_view(_SCRATCH.get("sat", tbytes, device), rows, ld, np.uint64) if scratch
+           else _device.empty((rows + 1, ld), np.uint64, device, f"a {rows + 1}x{cols + 1} integral table"))
+    out_r, out_c = rows - w + 1, cols - w + 1
+    outs = outs or alloc_outputs(kind, stats, out_r, out_c, device)
+    ws_bytes = int(lib.ssb_sat_swa_workspace_bytes(kind.abi_code, rows, cols))
+    ws = _SCRATCH.get("ws", ws_bytes, device)
+    rc = lib.ssb_sat_build_swa(_ptr(x), kind.abi_code, rows, cols, cols, _ptr(sat), ld, w, stat_mask(stats),
+                               _ptr(outs.get(StatKind.SUM)), _ptr(outs.get(StatKind.MEAN)), out_c, _ptr(ws),
+                               ws_bytes, _device.stream_ptr(device))
+    _lib.check(rc, "table + window sweep", (rows + 1) * (cols + 1) * 8)
+    return sat, ld, outs
+
+
 def fused(x, kind: ElemKind, rows: int, cols: int, w: int, stats, device, flag=None, outs=None, segments: int = 0):
     lib = _lib.load()
     out_r, out_c = rows - w + 1, cols - w + 1
@@ -191,6 +218,8 @@ def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto
     flag = new_flag(dev) if img.elem_kind is ElemKind.F32 else None
     if pipe == "fused":
         res = fused(x, img.elem_kind, rows, cols, w, stats, dev, flag=flag, outs=outs)
+    elif sweep_supported(img.elem_kind, w, stride, stats):
+        res = table_and_sweep(x, img.elem_kind, rows, cols, w, stats, dev, outs=outs, scratch=True)[2]
     else:
         need_sq = StatKind.STD in stats
         sat, sq, ld = build_tables(x, img.elem_kind, rows, cols, dev, squared=need_sq, flag=flag, scratch=True)

@@ -40,6 +40,11 @@ cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C,
 cudaError_t launch_window_eval_multi(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R,
                                      int64_t C, int64_t sat_ld, int nwin, const int64_t* ws, int mask, const WinOut* outs,
                                      cudaStream_t st);
+bool sat_sweep_supported(int dtype, int64_t w, int mask);
+int64_t sat_sweep_workspace_bytes(int dtype, int64_t R, int64_t C);
+void sat_sweep_plan_info(int dtype, int64_t R, int64_t C, int64_t w, int64_t* info);
+cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld,
+                             int64_t w, int mask, WinOut o, void* ws, cudaStream_t st);
 constexpr int64_t kFusedMaxWindow = 3072;
 
 static std::atomic<long long> g_launches{0};
@@ -219,6 +224,47 @@ int ssb_window_eval(const void* sat, const void* sat_sq, int in_dtype, int64_t r
   cudaError_t e = launch_window_eval(sat, sat_sq, in_dtype == SSB_F32, in_dtype, rows, cols, sat_ld, w, stride,
                                      stat_mask, o, as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_window_eval");
+}
+
+int ssb_sat_swa_supported(int in_dtype, int64_t w, int stat_mask) {
+  return valid_dtype(in_dtype) && sat_sweep_supported(in_dtype, w, stat_mask) ? 1 : 0;
+}
+
+int64_t ssb_sat_swa_workspace_bytes(int in_dtype, int64_t rows, int64_t cols) {
+  if (!valid_dtype(in_dtype) || in_dtype == SSB_F32 || rows < 1 || cols < 1) return -1;
+  return sat_sweep_workspace_bytes(in_dtype, rows, cols);
+}
+
+int ssb_sat_swa_plan(int in_dtype, int64_t rows, int64_t cols, int64_t w, int64_t* info4) {
+  if (!valid_dtype(in_dtype) || in_dtype == SSB_F32 || rows < 1 || cols < 1 || w < 1 || !info4)
+    return fail(SSB_EINVAL, "bad plan request");
+  sat_sweep_plan_info(in_dtype, rows, cols, w, info4);
+  return SSB_OK;
+}
+
+int ssb_sat_build_swa(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                      int64_t sat_ld, int64_t w, int stat_mask, void* out_sum, double* out_mean, int64_t out_ld,
+                      void* ws, int64_t ws_bytes, void* stream) {
+  int rc = check_image(in_dtype, rows, cols, in_ld);
+  if (rc) return rc;
+  if ((rc = check_window(rows, cols, w, 1))) return rc;
+  if ((rc = check_stats(in_dtype, stat_mask))) return rc;
+  if (!sat_sweep_supported(in_dtype, w, stat_mask))
+    return fail(SSB_EUNSUPPORTED, "table+sweep pass takes integer input, sum/mean and w <= 257 (dtype %d, w %lld)",
+                in_dtype, (long long)w);
+  if ((rc = check_aligned(in, "input raster"))) return rc;
+  if (!sat) return fail(SSB_EINVAL, "no table to write");
+  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
+  if (reinterpret_cast<uintptr_t>(sat) & 15) return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  if (((stat_mask & SSB_SUM) && !out_sum) || ((stat_mask & SSB_MEAN) && !out_mean))
+    return fail(SSB_EINVAL, "missing output buffer");
+  if (out_ld < cols - w + 1) return fail(SSB_EINVAL, "out_ld < output cols");
+  const int64_t need = sat_sweep_workspace_bytes(in_dtype, rows, cols);
+  if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  WinOut o{out_sum, out_mean, nullptr, out_ld};
+  cudaError_t e = launch_sat_sweep(in_dtype, in, rows, cols, in_ld, sat, sat_ld, w, stat_mask, o, ws,
+                                   as_stream(stream));
+  return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build_swa");
 }
 
 int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols,

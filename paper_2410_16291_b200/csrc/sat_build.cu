@@ -34,6 +34,7 @@
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
 #include "sat_tiles.cuh"
+#include "sat_plan.cuh"
 
 #ifndef SSB_SCAN_MINB
 #define SSB_SCAN_MINB 1
@@ -469,47 +470,7 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
 }
 
 // ---------------------------------------------------------------------------
-// host-side launch
-struct SatPlan {
-  int TW, nJ, nK;
-  int64_t SR, PR, PC;
-  // workspace offsets in elements of 8 bytes
-  int64_t off_rowtot, off_rowtot_sq, off_colp, off_colp_sq, off_srl, off_srl_sq, total;
-};
-
-inline int tw_for(int dtype) { return (dtype == IN_U8 || dtype == IN_U16) ? 512 : 256; }
-
-inline SatPlan make_sat_plan(int dtype, int64_t R, int64_t C, bool sq) {
-  SatPlan p{};
-  p.TW = tw_for(dtype);
-  p.PR = R + 1; p.PC = C + 1;
-  p.nJ = (int)((p.PC + p.TW - 1) / p.TW);
-  const int RB = 8;  // segment height is a multiple of every kernel's row block
-#ifndef SSB_TILES_PER_SM
-#define SSB_TILES_PER_SM 64
-#endif
-  const int64_t target_tiles = (int64_t)SSB_TILES_PER_SM * kNumSMs;  // warp tiles: ~4 waves of 16 warps per SM
-  int64_t wantK = (target_tiles + p.nJ - 1) / p.nJ;
-  int64_t SR = (p.PR + wantK - 1) / wantK;
-  SR = ((SR + RB - 1) / RB) * RB;
-#ifndef SSB_SR_CAP
-#define SSB_SR_CAP 512
-#endif
-  if (SR > SSB_SR_CAP) SR = SSB_SR_CAP;
-  if (SR < RB) SR = RB;
-  p.SR = SR;
-  p.nK = (int)((p.PR + SR - 1) / SR);
-  int64_t o = 0;
-  p.off_rowtot = o; o += (int64_t)p.nJ * p.PR;
-  p.off_rowtot_sq = o; if (sq) o += (int64_t)p.nJ * p.PR;
-  p.off_colp = o; o += (int64_t)p.nK * p.PC;
-  p.off_colp_sq = o; if (sq) o += (int64_t)p.nK * p.PC;
-  p.off_srl = o; o += (int64_t)p.nK * p.nJ;
-  p.off_srl_sq = o; if (sq) o += (int64_t)p.nK * p.nJ;
-  p.total = o;
-  return p;
-}
-
+// host-side launch (SatPlan / make_sat_plan: sat_plan.cuh)
 
 template <typename InT, bool SQ, int RBR, int WPC>
 cudaError_t launch_reduce_rw(const InT* x, int64_t R, int64_t C, int64_t in_ld, typename Elem<InT>::Acc* rowtot,
@@ -611,6 +572,14 @@ cudaError_t launch_sat_prepare(int dtype, const void* in, int64_t R, int64_t C, 
                                void* totals, void* totals_sq, int* nonfinite, cudaStream_t st) {
   const SatPlan p = make_sat_plan(dtype, R, C, sq);
 #define CALL_T(T, S) launch_sat_prepare_t<T, S>(in, R, C, in_ld, ws, totals, totals_sq, nonfinite, st, p)
+  SSB_SAT_DISPATCH(CALL_T)
+#undef CALL_T
+}
+
+// phases 1-2 on an explicit plan (the table+sweep pipeline uses taller segments)
+cudaError_t launch_sat_prepare_plan(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, bool sq, void* ws,
+                                    int* nonfinite, cudaStream_t st, const SatPlan& p) {
+#define CALL_T(T, S) launch_sat_prepare_t<T, S>(in, R, C, in_ld, ws, nullptr, nullptr, nonfinite, st, p)
   SSB_SAT_DISPATCH(CALL_T)
 #undef CALL_T
 }

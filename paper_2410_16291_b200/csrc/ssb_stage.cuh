@@ -66,10 +66,10 @@ __device__ __forceinline__ void shift_words(const uint32_t* w, uint32_t* o, int 
   for (int k = 0; k < NO; ++k) o[k] = __funnelshift_r(w[k + SW], w[k + SW + 1], sb);
 }
 
-// LB (multiple of 16) consecutive bytes starting at byte Q of a row buffer.
+// LB (multiple of 4) consecutive bytes starting at byte Q of a row buffer.
 template <int LB>
 __device__ __forceinline__ void lane_bytes(const unsigned char* rowbuf, int Q, uint32_t (&o)[LB / 4]) {
-  constexpr int NC = LB / 16 + 1, NO = LB / 4;
+  constexpr int NC = (LB + 15) / 16 + 1, NO = LB / 4;  // chunks covering LB bytes at any 16-byte phase
   const uint4* p = reinterpret_cast<const uint4*>(rowbuf + (Q & ~15));
   uint32_t w[NC * 4];
 #pragma unroll

@@ -156,6 +156,24 @@ def window_sum(sat: IntegralImage, top: int, left: int, w: int):
     return raw[0]
 
 
+def swa_with_table(img: ImageGrid, win: WindowSpec, stat: StatKind) -> tuple[IntegralImage, ResultGrid]:
+    """build_sat(img) and swa_integral(img, win, stat) from one pass over the raster.
+
+    The builder and sweep seams (integral.py:166-189) fused: the kernel that
+    writes a table row also emits the windows whose bottom corner row it is,
+    so the table is written once and never read back (ssb_sat_build_swa).
+    Integer rasters, sum/mean, stride 1, w <= 257; any other request builds
+    the table and then sweeps it (same results)."""
+    win.validate_for(img.rows, img.cols)
+    if not _engine.sweep_supported(img.elem_kind, win.w, win.stride, (stat,)):
+        return _build(img, False), _run_tables(img, [win], stat)[0]
+    kind = select_accum(img.elem_kind, img.rows, img.cols, False)
+    x, dev = _engine.device_input(img)
+    sat, ld, outs = _engine.table_and_sweep(x, img.elem_kind, img.rows, img.cols, win.w, (stat,), dev)
+    table = IntegralImage(sat, kind, (img.rows, img.cols), False, img.elem_kind, ld)
+    return table, ResultGrid(stat, _finish(img, (stat,), outs)[stat])
+
+
 def _finish(img: ImageGrid, stats, res) -> dict:
     out = {}
     for s in stats:
@@ -176,6 +194,11 @@ def _run_tables(img: ImageGrid, wins, stat: StatKind):
     x, dev = _engine.device_input(img)
     flag = _engine.new_flag(dev) if img.elem_kind is ElemKind.F32 else None
     sq_needed = needs_squares(stat)
+    if len(wins) == 1 and _engine.sweep_supported(img.elem_kind, wins[0].w, wins[0].stride, (stat,)):
+        # one window: table and sweep in one pass (the table stays in scratch)
+        _, _, outs = _engine.table_and_sweep(x, img.elem_kind, img.rows, img.cols, wins[0].w, (stat,), dev,
+                                             scratch=True)
+        return [ResultGrid(stat, _finish(img, (stat,), outs)[stat])]
     sat, sq, ld = _engine.build_tables(x, img.elem_kind, img.rows, img.cols, dev, squared=sq_needed, flag=flag,
                                        scratch=True)
     results = []

@@ -1,0 +1,157 @@
+"""GPU parity of the one-pass table + window sweep (ssb_sat_build_swa, csrc/sat_sweep.cu).
+
+The kernel writes the integral image and the stride-1 window sums/means in
+one pass.  Its table must be bit-identical to ssb_sat_build's (and to the
+oracle's restatement of build_sat, integral.py:109-116), and its outputs
+bit-identical to the oracle's swa (integral.py:141-189, stats.py:35-56) and to
+the two-kernel table pipeline (ssb_sat_build -> ssb_window_eval)."""
+
+from __future__ import annotations
+
+import zlib
+
+import numpy as np
+import pytest
+
+from oracle import satsweep_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2410_16291_b200 import _lib, build_ext
+
+    build_ext.build()
+    _lib.load()
+    import paper_2410_16291_b200 as mod
+
+    return mod
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+
+    return torch.device("cuda", 0)
+
+
+def host(t, dt):
+    from paper_2410_16291_b200 import _device
+
+    return _device.to_host(t, dt)
+
+
+def to_dev(a, dev):
+    from paper_2410_16291_b200 import _device
+
+    return _device.to_device(a, dev)
+
+
+def raster(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    if kind == "u8":
+        return rng.integers(0, 256, (rows, cols), dtype=np.uint8)
+    if kind == "u8mask":
+        return (rng.random((rows, cols)) < 0.05).astype(np.uint8)
+    if kind == "u16":
+        return rng.integers(0, 65536, (rows, cols), dtype=np.uint16)
+    return rng.integers(-(2**31), 2**31, (rows, cols), dtype=np.int64).astype(np.int32)
+
+
+def oracle_table(v: np.ndarray) -> np.ndarray:
+    t = O.build_table(v)
+    return t.view(np.uint64) if t.dtype == np.int64 else t
+
+
+def two_kernel(sb, x, kind, rows, cols, w, stats, dev):
+    from paper_2410_16291_b200 import _engine
+
+    sat, sq, ld = _engine.build_tables(x, kind, rows, cols, dev, squared=False)
+    outs = _engine.eval_tables(sat, sq, ld, kind, rows, cols, w, 1, stats, dev)
+    return sat, ld, outs
+
+
+def check_case(sb, dev, kind: str, rows: int, cols: int, w: int, seed: int, stats=("sum",)):
+    from paper_2410_16291_b200 import _engine
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    v = raster(kind, rows, cols, seed)
+    ek = ElemKind.from_dtype(v.dtype)
+    sk = tuple(StatKind.parse(s) for s in stats)
+    assert _engine.sweep_supported(ek, w, 1, sk)
+    x = to_dev(v, dev)
+    sat, ld, outs = _engine.table_and_sweep(x, ek, rows, cols, w, sk, dev)
+    got_t = host(sat[:, : cols + 1], np.uint64)
+    np.testing.assert_array_equal(got_t, oracle_table(v), err_msg=f"table {kind} {rows}x{cols} w={w}")
+    sat2, ld2, outs2 = two_kernel(sb, x, ek, rows, cols, w, sk, dev)
+    assert np.array_equal(got_t, host(sat2[:, : cols + 1], np.uint64))
+    for s, k in zip(stats, sk):
+        ref = O.swa(v, w, s)
+        dt = np.float64 if s == "mean" else (np.int64 if kind == "i32" else np.uint64)
+        got = host(outs[k], dt)
+        np.testing.assert_array_equal(got, ref, err_msg=f"{s} {kind} {rows}x{cols} w={w}")
+        np.testing.assert_array_equal(got, host(outs2[k], dt))
+
+
+@pytest.mark.parametrize("kind", ["u8", "u8mask", "u16", "i32"])
+@pytest.mark.parametrize("shape,w", [((1, 1), 1), ((7, 5), 3), ((300, 517), 17), ((260, 1030), 256),
+                                     ((257, 257), 257), ((600, 1600), 2), ((520, 2200), 255)])
+def test_sweep_shapes(sb, dev, kind, shape, w):
+    if kind == "u16" and w > 256:
+        pytest.skip("u16 takes w <= 256 on this kernel (u32 window sums)")
+    check_case(sb, dev, kind, *shape, w, seed=zlib.crc32(f"{kind}{shape}{w}".encode()))
+
+
+@pytest.mark.parametrize("kind", ["u8", "u16", "i32"])
+def test_sweep_multi_segment(sb, dev, kind):
+    """Rows span several 2048-row segments: every segment after the first warms its
+    vertical sums up over the w rows above it."""
+    check_case(sb, dev, kind, 4500, 700, 200, seed=11, stats=("sum", "mean"))
+
+
+@pytest.mark.parametrize("w", [1, 64, 256, 257])
+def test_sweep_mean(sb, dev, w):
+    check_case(sb, dev, "u8", 2300, 1100, w, seed=w, stats=("mean",))
+
+
+def test_sweep_api(sb, dev):
+    """swa_with_table returns build_sat's table and swa's result; swa(pipeline='table')
+    routes here for eligible requests, with the reference's result dtype."""
+    v = raster("u8", 1200, 900, 3)
+    x = to_dev(v, dev)
+    sat, res = sb.swa_with_table(sb.ImageGrid(x), sb.WindowSpec(100), sb.StatKind.SUM)
+    np.testing.assert_array_equal(sat.table, oracle_table(v))
+    np.testing.assert_array_equal(host(res.values, np.uint64), O.swa(v, 100, "sum"))
+    hsat, hres = sb.swa_with_table(sb.ImageGrid(v), sb.WindowSpec(100), sb.StatKind.MEAN)
+    assert hres.values.dtype == np.float64
+    np.testing.assert_array_equal(hres.values, O.swa(v, 100, "mean"))
+    assert sb.window_sum(hsat, 5, 7, 100) == O.swa(v, 100, "sum")[5, 7]
+    np.testing.assert_array_equal(sb.swa(v, 100, "sum", pipeline="table"), O.swa(v, 100, "sum"))
+    # ineligible requests (std, f32, wide windows) take build + sweep with the same contract
+    f = np.random.default_rng(4).random((300, 400), dtype=np.float32)
+    fsat, fres = sb.swa_with_table(sb.ImageGrid(f), sb.WindowSpec(20), sb.StatKind.STD)
+    np.testing.assert_allclose(fres.values, O.swa(f, 20, "std"), rtol=1e-6, atol=1e-9)
+    np.testing.assert_array_equal(fsat.table, O.build_table(f))
+    wsat, wres = sb.swa_with_table(sb.ImageGrid(v), sb.WindowSpec(300), sb.StatKind.SUM)
+    np.testing.assert_array_equal(wres.values, O.swa(v, 300, "sum"))
+
+
+def test_sweep_c5_band(sb, dev, hashes):
+    """A reference-hashed C5 band (rows [34000, 34512) of the w=256 result)."""
+    from conftest import digest
+    from paper_2410_16291_b200 import _engine, synthetic
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    lo, hi = 34000, 34512
+    v = synthetic.c5(lo, hi + 255)
+    x = to_dev(v, dev)
+    sat, ld, outs = _engine.table_and_sweep(x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev)
+    assert digest(host(outs[StatKind.SUM], np.uint64)) == hashes[f"C5_sum_w256_rows{lo}_{hi}"]
+    sat2, _, _ = two_kernel(sb, x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev)
+    import torch
+
+    assert bool(torch.equal(sat, sat2))
