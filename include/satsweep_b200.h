@@ -128,14 +128,17 @@ int ssb_sat_build_lookback(const void* in, int in_dtype, int64_t rows, int64_t c
                            void* sat_sq, int64_t sat_ld, const void* carry, const void* carry_sq, void* ws,
                            int64_t ws_bytes, void* stream);
 
-/* Integral image AND its stride-1 window statistics in one pass over the
- * raster: writes the same table as ssb_sat_build (no carry, no squares) and
- * the same outputs as ssb_window_eval on it, without reading the table back
- * (build_sat + sweep_window_sums + finalize, integral.py:109-116, :141-189,
- * fused at the builder/sweep seams integral.py:166-189).  Integer input only;
+/* Integral image AND its stride-1 window statistics (build_sat +
+ * sweep_window_sums + finalize, integral.py:109-116, :141-189, fused at the
+ * builder/sweep seams integral.py:166-189): writes the same table as
+ * ssb_sat_build (no carry, no squares) and the same outputs as
+ * ssb_window_eval on it, without reading the table back.  Integer input only;
  * stats SUM and/or MEAN; w <= 257 (u16: w <= 256).  ssb_sat_swa_supported
- * reports whether a request qualifies (1) or not (0); its workspace is
- * ssb_sat_swa_workspace_bytes. */
+ * reports whether a request qualifies (1) or not (0); the workspace is
+ * ssb_sat_swa_workspace_bytes.  ssb_sat_build_swa runs the faster pipeline
+ * on B200 (table build, then the windows from the raster by the fused
+ * kernel); ssb_sat_build_swa_onepass runs the one-pass kernel, whose table
+ * writer also emits the windows (same results; A/B). */
 int ssb_sat_swa_supported(int in_dtype, int64_t w, int stat_mask);
 int64_t ssb_sat_swa_workspace_bytes(int in_dtype, int64_t rows, int64_t cols);
 /* Tiling of ssb_sat_build_swa: info4 = {warp strips, sweep segment height
@@ -144,6 +147,9 @@ int ssb_sat_swa_plan(int in_dtype, int64_t rows, int64_t cols, int64_t w, int64_
 int ssb_sat_build_swa(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
                       int64_t sat_ld, int64_t w, int stat_mask, void* out_sum, double* out_mean, int64_t out_ld,
                       void* ws, int64_t ws_bytes, void* stream);
+int ssb_sat_build_swa_onepass(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                              int64_t sat_ld, int64_t w, int stat_mask, void* out_sum, double* out_mean,
+                              int64_t out_ld, void* ws, int64_t ws_bytes, void* stream);
 
 /* Several window sizes (stride 1) from one set of tables. */
 int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols,

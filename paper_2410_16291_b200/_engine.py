@@ -150,11 +150,12 @@ def sweep_supported(kind: ElemKind, w: int, stride: int, stats) -> bool:
 
 
 def table_and_sweep(x, kind: ElemKind, rows: int, cols: int, w: int, stats, device, *, outs=None,
-                    scratch: bool = False):
-    """Integral image AND its stride-1 window stats in one pass (ssb_sat_build_swa).
+                    scratch: bool = False, onepass: bool = False):
+    """Integral image AND its stride-1 window stats (ssb_sat_build_swa).
 
     Same table as build_tables and same outputs as eval_tables on it, but the
-    table is never read back.  Returns (sat, sat_ld, outs)."""
+    table is never read back.  ``onepass`` selects the one-pass kernel
+    (ssb_sat_build_swa_onepass).  Returns (sat, sat_ld, outs)."""
     lib = _lib.load()
     ld = sat_ld_for(cols)
     tbytes = (rows + 1) * ld * 8
@@ -164,9 +165,10 @@ def table_and_sweep(x, kind: ElemKind, rows: int, cols: int, w: int, stats, devi
     outs = outs or alloc_outputs(kind, stats, out_r, out_c, device)
     ws_bytes = int(lib.ssb_sat_swa_workspace_bytes(kind.abi_code, rows, cols))
     ws = _SCRATCH.get("ws", ws_bytes, device)
-    rc = lib.ssb_sat_build_swa(_ptr(x), kind.abi_code, rows, cols, cols, _ptr(sat), ld, w, stat_mask(stats),
-                               _ptr(outs.get(StatKind.SUM)), _ptr(outs.get(StatKind.MEAN)), out_c, _ptr(ws),
-                               ws_bytes, _device.stream_ptr(device))
+    fn = lib.ssb_sat_build_swa_onepass if onepass else lib.ssb_sat_build_swa
+    rc = fn(_ptr(x), kind.abi_code, rows, cols, cols, _ptr(sat), ld, w, stat_mask(stats),
+            _ptr(outs.get(StatKind.SUM)), _ptr(outs.get(StatKind.MEAN)), out_c, _ptr(ws), ws_bytes,
+            _device.stream_ptr(device))
     _lib.check(rc, "table + window sweep", (rows + 1) * (cols + 1) * 8)
     return sat, ld, outs
 

@@ -47,6 +47,8 @@ _SIGS = {
     "ssb_sat_swa_workspace_bytes": (_i64, [_int, _i64, _i64]),
     "ssb_sat_swa_plan": (_int, [_int, _i64, _i64, _i64, ctypes.POINTER(_i64)]),
     "ssb_sat_build_swa": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _vp, _i64, _vp, _i64, _vp]),
+    "ssb_sat_build_swa_onepass": (
+        _int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _vp, _i64, _vp, _i64, _vp]),
     "ssb_window_eval": (_int, [_vp, _vp, _int, _i64, _i64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _i64, _vp]),
     "ssb_window_eval_multi": (
         _int,

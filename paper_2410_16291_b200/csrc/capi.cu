@@ -44,7 +44,7 @@ bool sat_sweep_supported(int dtype, int64_t w, int mask);
 int64_t sat_sweep_workspace_bytes(int dtype, int64_t R, int64_t C);
 void sat_sweep_plan_info(int dtype, int64_t R, int64_t C, int64_t w, int64_t* info);
 cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld,
-                             int64_t w, int mask, WinOut o, void* ws, cudaStream_t st);
+                             int64_t w, int mask, WinOut o, void* ws, cudaStream_t st, bool onepass);
 constexpr int64_t kFusedMaxWindow = 3072;
 
 static std::atomic<long long> g_launches{0};
@@ -242,7 +242,9 @@ int ssb_sat_swa_plan(int in_dtype, int64_t rows, int64_t cols, int64_t w, int64_
   return SSB_OK;
 }
 
-int ssb_sat_build_swa(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+}  // extern "C"
+
+static int sat_build_swa_impl(bool onepass, const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
                       int64_t sat_ld, int64_t w, int stat_mask, void* out_sum, double* out_mean, int64_t out_ld,
                       void* ws, int64_t ws_bytes, void* stream) {
   int rc = check_image(in_dtype, rows, cols, in_ld);
@@ -263,8 +265,24 @@ int ssb_sat_build_swa(const void* in, int in_dtype, int64_t rows, int64_t cols, 
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
   WinOut o{out_sum, out_mean, nullptr, out_ld};
   cudaError_t e = launch_sat_sweep(in_dtype, in, rows, cols, in_ld, sat, sat_ld, w, stat_mask, o, ws,
-                                   as_stream(stream));
+                                   as_stream(stream), onepass);
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build_swa");
+}
+
+extern "C" {
+
+int ssb_sat_build_swa(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                      int64_t sat_ld, int64_t w, int stat_mask, void* out_sum, double* out_mean, int64_t out_ld,
+                      void* ws, int64_t ws_bytes, void* stream) {
+  return sat_build_swa_impl(false, in, in_dtype, rows, cols, in_ld, sat, sat_ld, w, stat_mask, out_sum, out_mean,
+                            out_ld, ws, ws_bytes, stream);
+}
+
+int ssb_sat_build_swa_onepass(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, void* sat,
+                              int64_t sat_ld, int64_t w, int stat_mask, void* out_sum, double* out_mean,
+                              int64_t out_ld, void* ws, int64_t ws_bytes, void* stream) {
+  return sat_build_swa_impl(true, in, in_dtype, rows, cols, in_ld, sat, sat_ld, w, stat_mask, out_sum, out_mean,
+                            out_ld, ws, ws_bytes, stream);
 }
 
 int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int64_t rows, int64_t cols,

@@ -366,8 +366,12 @@ bool sat_sweep_supported(int dtype, int64_t w, int mask) {
   }
 }
 
+int64_t sat_workspace_bytes(int dtype, int64_t R, int64_t C, bool sq);
+
 int64_t sat_sweep_workspace_bytes(int dtype, int64_t R, int64_t C) {
-  return make_sat_plan(dtype, R, C, false).total * 8;
+  const int64_t one = make_sat_plan(dtype, R, C, false).total * 8;
+  const int64_t two = sat_workspace_bytes(dtype, R, C, false);  // includes the look-back build's needs
+  return one > two ? one : two;
 }
 
 void sat_sweep_plan_info(int dtype, int64_t R, int64_t C, int64_t w, int64_t* info) {
@@ -400,9 +404,34 @@ cudaError_t launch_sweep_t(const void* in, int64_t R, int64_t C, int64_t in_ld, 
   return cudaGetLastError();
 }
 
-// reduce + carries (sat_build.cu phases 1-2), then the table+sweep kernel
+cudaError_t launch_sat_build(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, void* sat_sq,
+                             int64_t sat_ld, const void* carry, const void* carry_sq, void* ws, int* nonfinite,
+                             cudaStream_t st);
+cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
+                                WinOut o, int* nonfinite, int nK, cudaStream_t st);
+
+// Default: the table build (reduce-then-scan, sat_build.cu) followed by the
+// fused window kernel (window_fused.cu), which evaluates the windows from the
+// raster instead of reading the table back: measured at C5 (B200) 21.0 ms vs
+// 23.3 ms for the one-pass kernel above and 24.7 ms for build + corner sweep.
+// ssb_sat_build_swa_onepass (or SSB_SWA_PATH=onepass) runs the one-pass kernel.
+static bool swa_onepass_env() {
+  static const bool one = [] {
+    const char* e = getenv("SSB_SWA_PATH");
+    return e && e[0] == 'o';
+  }();
+  return one;
+}
+
+// table + window statistics: the table build then the fused window kernel, or
+// reduce + carries then the one-pass table+sweep kernel
 cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld,
-                             int64_t w, int mask, WinOut o, void* ws, cudaStream_t st) {
+                             int64_t w, int mask, WinOut o, void* ws, cudaStream_t st, bool onepass) {
+  if (!onepass && !swa_onepass_env()) {
+    cudaError_t e = launch_sat_build(dtype, in, R, C, in_ld, sat, nullptr, sat_ld, nullptr, nullptr, ws, nullptr, st);
+    if (e != cudaSuccess) return e;
+    return launch_window_fused(in, dtype, R, C, in_ld, w, mask, o, nullptr, 0, st);
+  }
   const SweepPlan sp = make_sweep_plan(dtype, R, C, w);
   cudaError_t e = launch_sat_prepare_plan(dtype, in, R, C, in_ld, false, ws, nullptr, st, sp.p);
   if (e != cudaSuccess) return e;

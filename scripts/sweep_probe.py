@@ -24,8 +24,8 @@ ws = _device.empty((max(wsb, int(lib.ssb_sat_workspace_bytes(0, rows, cols, 0)))
 st = torch.cuda.current_stream(dev).cuda_stream
 
 
-def sweep():
-    _lib.check(lib.ssb_sat_build_swa(x.data_ptr(), 0, rows, cols, cols, sat.data_ptr(), ld, w, 1, out.data_ptr(),
+def sweep(fn=None):
+    _lib.check((fn or lib.ssb_sat_build_swa)(x.data_ptr(), 0, rows, cols, cols, sat.data_ptr(), ld, w, 1, out.data_ptr(),
                                      None, cols - w + 1, ws.data_ptr(), ws.numel(), st))
 
 
@@ -49,16 +49,31 @@ def timeit(fn, n=10):
     return a.elapsed_time(b) / n
 
 
+def prep():
+    _lib.check(lib.ssb_sat_prepare(x.data_ptr(), 0, rows, cols, cols, 0, ws.data_ptr(), ws.numel(), None, None, None,
+                                   st))
+
+
+import os
+
+def onepass():
+    sweep(lib.ssb_sat_build_swa_onepass)
+
+
+if os.environ.get("PROBE_FAST"):  # tuning: one-pass and its reduce phase only
+    a, b = timeit(onepass), timeit(prep)
+    print(f"one-pass {a:.3f} ms  reduce+carries {b:.3f} ms  sweep kernel {a - b:.3f} ms  {rows * cols / a / 1e6:.1f} Gpx/s")
+    sys.exit(0)
 two()
 ref = out.clone()
 reft = sat.view(torch.int64).sum(dim=1)  # per-row checksums (the table itself is 44 GiB)
 sat.zero_()
-sweep()
+onepass()
 torch.cuda.synchronize()
 print("equal outputs:", bool(torch.equal(out, ref)), "equal table row checksums:",
       bool(torch.equal(sat.view(torch.int64).sum(dim=1), reft)))
 del ref, reft
-for name, fn in (("two-kernel", two), ("one-pass", sweep)):
+for name, fn in (("build+sweep", two), ("one-pass", onepass), ("build+fused (ssb_sat_build_swa)", sweep)):
     ms = timeit(fn)
     px = rows * cols
     b = px + (rows + 1) * (cols + 1) * 8 + (rows - w + 1) * (cols - w + 1) * 8

@@ -75,7 +75,7 @@ def two_kernel(sb, x, kind, rows, cols, w, stats, dev):
     return sat, ld, outs
 
 
-def check_case(sb, dev, kind: str, rows: int, cols: int, w: int, seed: int, stats=("sum",)):
+def check_case(sb, dev, kind: str, rows: int, cols: int, w: int, seed: int, stats=("sum",), onepass=False):
     from paper_2410_16291_b200 import _engine
     from paper_2410_16291_b200.grid import ElemKind, StatKind
 
@@ -84,7 +84,7 @@ def check_case(sb, dev, kind: str, rows: int, cols: int, w: int, seed: int, stat
     sk = tuple(StatKind.parse(s) for s in stats)
     assert _engine.sweep_supported(ek, w, 1, sk)
     x = to_dev(v, dev)
-    sat, ld, outs = _engine.table_and_sweep(x, ek, rows, cols, w, sk, dev)
+    sat, ld, outs = _engine.table_and_sweep(x, ek, rows, cols, w, sk, dev, onepass=onepass)
     got_t = host(sat[:, : cols + 1], np.uint64)
     np.testing.assert_array_equal(got_t, oracle_table(v), err_msg=f"table {kind} {rows}x{cols} w={w}")
     sat2, ld2, outs2 = two_kernel(sb, x, ek, rows, cols, w, sk, dev)
@@ -97,25 +97,28 @@ def check_case(sb, dev, kind: str, rows: int, cols: int, w: int, seed: int, stat
         np.testing.assert_array_equal(got, host(outs2[k], dt))
 
 
+@pytest.mark.parametrize("onepass", [False, True], ids=["build+fused", "onepass"])
 @pytest.mark.parametrize("kind", ["u8", "u8mask", "u16", "i32"])
 @pytest.mark.parametrize("shape,w", [((1, 1), 1), ((7, 5), 3), ((300, 517), 17), ((260, 1030), 256),
                                      ((257, 257), 257), ((600, 1600), 2), ((520, 2200), 255)])
-def test_sweep_shapes(sb, dev, kind, shape, w):
+def test_sweep_shapes(sb, dev, kind, shape, w, onepass):
     if kind == "u16" and w > 256:
-        pytest.skip("u16 takes w <= 256 on this kernel (u32 window sums)")
-    check_case(sb, dev, kind, *shape, w, seed=zlib.crc32(f"{kind}{shape}{w}".encode()))
+        pytest.skip("u16 takes w <= 256 (u32 window sums)")
+    check_case(sb, dev, kind, *shape, w, seed=zlib.crc32(f"{kind}{shape}{w}".encode()), onepass=onepass)
 
 
+@pytest.mark.parametrize("onepass", [False, True], ids=["build+fused", "onepass"])
 @pytest.mark.parametrize("kind", ["u8", "u16", "i32"])
-def test_sweep_multi_segment(sb, dev, kind):
-    """Rows span several 2048-row segments: every segment after the first warms its
-    vertical sums up over the w rows above it."""
-    check_case(sb, dev, kind, 4500, 700, 200, seed=11, stats=("sum", "mean"))
+def test_sweep_multi_segment(sb, dev, kind, onepass):
+    """Rows span many sweep segments: every segment after the first warms its
+    vertical sums up over the w rows above it (one-pass kernel)."""
+    check_case(sb, dev, kind, 4500, 700, 200, seed=11, stats=("sum", "mean"), onepass=onepass)
 
 
+@pytest.mark.parametrize("onepass", [False, True], ids=["build+fused", "onepass"])
 @pytest.mark.parametrize("w", [1, 64, 256, 257])
-def test_sweep_mean(sb, dev, w):
-    check_case(sb, dev, "u8", 2300, 1100, w, seed=w, stats=("mean",))
+def test_sweep_mean(sb, dev, w, onepass):
+    check_case(sb, dev, "u8", 2300, 1100, w, seed=w, stats=("mean",), onepass=onepass)
 
 
 def test_sweep_api(sb, dev):
@@ -149,9 +152,11 @@ def test_sweep_c5_band(sb, dev, hashes):
     lo, hi = 34000, 34512
     v = synthetic.c5(lo, hi + 255)
     x = to_dev(v, dev)
-    sat, ld, outs = _engine.table_and_sweep(x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev)
-    assert digest(host(outs[StatKind.SUM], np.uint64)) == hashes[f"C5_sum_w256_rows{lo}_{hi}"]
-    sat2, _, _ = two_kernel(sb, x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev)
     import torch
 
-    assert bool(torch.equal(sat, sat2))
+    sat2, _, _ = two_kernel(sb, x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev)
+    for onepass in (False, True):
+        sat, ld, outs = _engine.table_and_sweep(x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev,
+                                                onepass=onepass)
+        assert digest(host(outs[StatKind.SUM], np.uint64)) == hashes[f"C5_sum_w256_rows{lo}_{hi}"]
+        assert bool(torch.equal(sat, sat2))
