@@ -388,6 +388,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   if ((rc = check_window(rows, cols, w, stride))) return rc;
   if ((rc = check_stats(in_dtype, stat_mask))) return rc;
   if (pipeline == SSB_PIPE_FUSED && (stride != 1 || w > kFusedMaxWindow)) pipeline = SSB_PIPE_TABLE;
+  const bool sweep_ok = stride == 1 && sat_sweep_supported(in_dtype, w, stat_mask);
   const bool sq = (stat_mask & SSB_STD) != 0;
   const int es = elem_size(in_dtype);
   const int64_t out_r = (rows - w) / stride + 1, out_c = (cols - w) / stride + 1;
@@ -459,7 +460,9 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if ((e = cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es, (size_t)nr,
                                cudaMemcpyHostToDevice, s.st)) != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
     WinOut o{s.o_sum, reinterpret_cast<double*>(s.o_mean), reinterpret_cast<double*>(s.o_std), out_c};
-    if (pipeline == SSB_PIPE_TABLE) {
+    if (pipeline == SSB_PIPE_TABLE && sweep_ok) {  // table + windows without reading the table back
+      e = launch_sat_sweep(in_dtype, s.in, nr, cols, cols, s.sat, sat_ld, w, stat_mask, o, s.ws, s.st, false);
+    } else if (pipeline == SSB_PIPE_TABLE) {
       e = launch_sat_build(in_dtype, s.in, nr, cols, cols, s.sat, s.sq, sat_ld, nullptr, nullptr, s.ws, d_flag, s.st);
       if (e == cudaSuccess)
         e = launch_window_eval(s.sat, s.sq, in_dtype == SSB_F32, in_dtype, nr, cols, sat_ld, w, stride, stat_mask, o, s.st);
