@@ -236,26 +236,32 @@ def main() -> None:
             return x_own
         return shard.halo_exchange(x_own, rows, W, 1, group, storage=storage)
 
-    ev = {k: [] for k in ("build", "windows")}
+    ev = {k: [] for k in ("build", "windows", "group")}
+
+    side = torch.cuda.Stream(dev)
 
     def step(record: bool):
         x = get_x()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e2 = torch.cuda.Event(enable_timing=True)
+        e0, e1, f0, f1, ej = (torch.cuda.Event(enable_timing=True) for _ in range(5))
+        # ssb_sat_build_swa's launches with events around each kernel group: the
+        # table build (reduce-then-scan; SSB_SAT_PATH=one selects the
+        # single-pass look-back kernel) on the step's stream and, concurrently
+        # on a forked side stream, the window sums from the raster; joined
         e0.record(stream)
-        # ssb_sat_build_swa's launches, with an event between them: the table
-        # build (reduce-then-scan; SSB_SAT_PATH=one selects the single-pass
-        # look-back kernel), then the window sums from the raster
+        side.wait_event(e0)
         _lib.check(lib.ssb_sat_build(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), None, ld, None,
                                      None, ws.data_ptr(), ws_bytes, None, sptr))
         e1.record(stream)
+        f0.record(side)
         _lib.check(lib.ssb_window_fused(x.data_ptr(), kind.abi_code, nr, COLS, COLS, W, _lib.SUM, out.data_ptr(),
-                                        None, None, out_c, None, 0, sptr))
-        e2.record(stream)
+                                        None, None, out_c, None, 0, side.cuda_stream))
+        f1.record(side)
+        stream.wait_event(f1)
+        ej.record(stream)
         if record:
             ev["build"].append((e0, e1))
-            ev["windows"].append((e1, e2))
+            ev["windows"].append((f0, f1))
+            ev["group"].append((e0, ej))
 
     def barrier():
         if world > 1:
@@ -292,18 +298,24 @@ def main() -> None:
     px_in = nr * COLS
     tab_bytes = (nr + 1) * (COLS + 1) * 8
     out_bytes = n_out * out_c * 8
+    # the step's two kernel groups run concurrently, so the roofline is taken on
+    # the group: each kernel's algorithmic bytes (sat_build: image read + table
+    # write; window_fused: image read + window sums write) over the group's
+    # duration (fork event -> join event on the step's stream)
     kernels = {
         "sat_build (image read + table write)": (px_in + tab_bytes, phase_ms["build"]),
         "window_fused (image read + window sums write)": (px_in + out_bytes, phase_ms["windows"]),
     }
     pk = peaks()
-    dom = max(kernels, key=lambda k: kernels[k][1])
-    dom_bytes, dom_ms = kernels[dom]
+    dom = "sat_build || window_fused (concurrent kernel group of one step)"
+    dom_bytes, dom_ms = sum(b for b, _ in kernels.values()), phase_ms["group"]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     tfile = REPO / "profiles" / "traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(dom.split(" ")[0])
+        tr = json.loads(tfile.read_text())
+        if "sat_build" in tr and "window_fused" in tr:
+            traffic = tr["sat_build"] + tr["window_fused"]
     b_alg = px_in + tab_bytes + out_bytes  # every distinct array read or written once
     b_mat = px_in + 2 * tab_bytes + out_bytes  # the reference structure (table written, then read back)
     value = rows * COLS / (ms_step * 1e-3) / 1e9
@@ -314,19 +326,20 @@ def main() -> None:
         "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded C5 recipe, synthetic.py)",
         "config": {"workload": "C5 70000x85000 u8 mask, integral image (u64) + window sum w=256 stride 1",
-                   "pipeline": "table + windows (ssb_sat_build -> ssb_window_fused = ssb_sat_build_swa)",
+                   "pipeline": "table + windows (ssb_sat_build || ssb_window_fused on a forked stream = "
+                               "ssb_sat_build_swa)",
                    "parallelism": f"rowband{world}",
                    "sat_path": "single-pass decoupled look-back" if os.environ.get("SSB_SAT_PATH", "").startswith("o")
                    else "reduce-then-scan",
                    "l2": "inputs 5.95 GB >> 126 MB L2; no flush needed", "gen_s": round(gen_s, 1)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": dom,
-                     "peak_source": pk["source"]},
+                     "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms, "peak_source": pk["source"]},
         "pipeline_roofline": {"bytes_per_step": b_alg, "achieved_gbs": b_alg / (ms_step * 1e-3) / 1e9,
                               "frac": b_alg / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"],
                               "bytes": "image read + table write + window sums write, each once"},
         "phases_ms": phase_ms,
-        "phase_gbs": {k: b / (ms * 1e-3) / 1e9 for k, (b, ms) in kernels.items()},
+        "phase_gbs": {k: b / (ms * 1e-3) / 1e9 for k, (b, ms) in kernels.items()},  # in context (overlapping)
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -359,12 +372,18 @@ def main() -> None:
                                                      W, _lib.SUM, out.data_ptr(), None, out_c, ws.data_ptr(),
                                                      ws_bytes, sptr))
 
-        for name, fn, b in (("corner_sweep_pipeline", sweep_step, b_mat), ("onepass_pipeline", onepass_step, b_alg)):
+        def swa_call_step():
+            _lib.check(lib.ssb_sat_build_swa(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), ld, W,
+                                             _lib.SUM, out.data_ptr(), None, out_c, ws.data_ptr(), ws_bytes, sptr))
+
+        for name, fn, b in (("corner_sweep_pipeline", sweep_step, b_mat), ("onepass_pipeline", onepass_step, b_alg),
+                            ("ssb_sat_build_swa_call", swa_call_step, b_alg)):
             ms = time_steps(fn)
             result[name] = {"value": rows * COLS / (ms * 1e-3) / 1e9, "ms_per_step": ms, "bytes_per_step": b,
                             "roofline_frac": b / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
         result["corner_sweep_pipeline"]["api"] = "ssb_sat_build -> ssb_window_eval (table read back)"
         result["onepass_pipeline"]["api"] = "ssb_sat_build_swa_onepass"
+        result["ssb_sat_build_swa_call"]["api"] = "ssb_sat_build_swa (the headline step as one C-ABI call)"
     except Exception as exc:  # pragma: no cover - reporting only
         result["corner_sweep_pipeline"] = {"error": str(exc)}
 

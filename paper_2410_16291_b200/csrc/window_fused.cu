@@ -20,11 +20,19 @@
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
 
+#ifndef SSB_FUSED_STAGES
+#define SSB_FUSED_STAGES 2
+#endif
+#ifndef SSB_FUSED_OUT_UNROLL
+#define SSB_FUSED_OUT_UNROLL 4
+#endif
 #ifndef SSB_FUSED_MINB
 #define SSB_FUSED_MINB 3
 #endif
 
 namespace ssb {
+
+constexpr int kFusedOutUnroll = SSB_FUSED_OUT_UNROLL;  // outputs in flight per lane in the store loop
 
 template <typename InT, int E>
 __device__ __forceinline__ void load_cols(const InT* __restrict__ p, int64_t c0, int64_t C, bool vec_ok, InT (&x)[E]) {
@@ -239,6 +247,86 @@ cudaError_t launch_fused_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
 }
 
 // ---------------------------------------------------------------------------
+// uint8 sums from packed vertical sums (V[2g] = columns 4g, 4g+2 and V[2g+1] =
+// columns 4g+1, 4g+3 as 16-bit halves).  One output row of a strip:
+//   * the lane total and the running prefix take one DP2A per column
+//     (a.lo16 * b.byte0 + a.hi16 * b.byte1 + c extracts and adds in one step);
+//   * P[u] is stored at word pp(u + d), pp(v) = v + 2 (v >> 6): even v are
+//     8-byte aligned, and d = 1 when the row's first output is not 16-byte
+//     aligned in global memory, so every output pair (j, j + 1) that is 16-byte aligned in global memory
+//     reads its two P words with one 64-bit shared load per operand;
+//   * pairs leave as one 16-byte streaming store.
+__device__ __forceinline__ int pp(int v) { return v + 2 * (v >> 6); }
+
+#ifndef SSB_FUSED_ST
+#define SSB_FUSED_ST 0
+#endif
+// 16-byte output store: streaming (evict-first) by default; tuning variants
+__device__ __forceinline__ void st_pair(uint64_t* p, uint64_t a, uint64_t b) {
+#if SSB_FUSED_ST == 0
+  st_cs2(p, a, b);
+#elif SSB_FUSED_ST == 1
+  asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+#else
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+#endif
+}
+
+template <int E>
+__device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint32_t* P, int64_t gb,
+                                                uint64_t* __restrict__ out, int nout, int w, int lane) {
+  const int d = (int)((reinterpret_cast<uintptr_t>(out + gb) >> 3) & 1);  // 16-byte phase of output 0
+  uint32_t tot = 0u;
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i) tot = __dp2a_lo(V[i], 0x0101u, tot);
+  uint32_t run = warp_incl_scan(tot, lane) - tot;
+  const int ub = lane * E + 1 + d;  // pp argument of this lane's first P entry
+#pragma unroll
+  for (int q = 0; q < E / 4; ++q) {
+    const uint32_t r0 = __dp2a_lo(V[2 * q], 0x0001u, run);
+    const uint32_t r1 = __dp2a_lo(V[2 * q + 1], 0x0001u, r0);
+    const uint32_t r2 = __dp2a_lo(V[2 * q], 0x0100u, r1);
+    const uint32_t r3 = __dp2a_lo(V[2 * q + 1], 0x0100u, r2);
+    P[pp(ub + 4 * q)] = r0;
+    P[pp(ub + 4 * q + 1)] = r1;
+    P[pp(ub + 4 * q + 2)] = r2;
+    P[pp(ub + 4 * q + 3)] = r3;
+    run = r3;
+  }
+  if (lane == 0) P[pp(d)] = 0u;
+  __syncwarp();
+  uint64_t* orow = out + gb;
+  if (lane == 0) {
+    if (d) orow[0] = (uint64_t)(P[pp(w + 1)] - P[pp(1)]);                         // leading single
+    if ((nout - d) & 1) orow[nout - 1] = (uint64_t)(P[pp(nout - 1 + w + d)] - P[pp(nout - 1 + d)]);  // trailing
+  }
+  const int npair = (nout - d) >> 1;
+  // pair m: outputs j = d + 2m, d + 2m + 1; P words at pp(j + d) (even) and pp(j + w + d)
+  const int va = 2 * lane + 2 * d, vb = va + w;
+  const uint32_t* pa = P + pp(va);
+  uint64_t* dst = orow + d + 2 * lane;
+  const int nq = (npair - lane + 31) >> 5;
+  if ((w & 1) == 0) {
+    const uint32_t* pb = P + pp(vb);
+#pragma unroll 4
+    for (int qq = 0; qq < nq; ++qq) {
+      const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
+      const uint2 B = *reinterpret_cast<const uint2*>(pb + 66 * qq);
+      st_pair(dst + 64 * qq, (uint64_t)(B.x - A.x), (uint64_t)(B.y - A.y));
+    }
+  } else {
+    const uint32_t* pb0 = P + pp(vb);
+    const uint32_t* pb1 = P + pp(vb + 1);
+#pragma unroll 4
+    for (int qq = 0; qq < nq; ++qq) {
+      const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
+      st_pair(dst + 64 * qq, (uint64_t)(pb0[66 * qq] - A.x), (uint64_t)(pb1[66 * qq] - A.y));
+    }
+  }
+  __syncwarp();  // P is rewritten by the next row
+}
+
+// ---------------------------------------------------------------------------
 // Strip kernel (default).  Every warp owns one output-column strip of TWo = NV
 // - w + 1 columns (NV = 32 E image columns incl. the w-1 halo) and one segment
 // of output rows, and sweeps it top to bottom on its own 2-deep TMA ring
@@ -257,10 +345,11 @@ template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ>
 struct StripSmem {
   static constexpr int NV = 32 * E;
   static constexpr int ROWB = NV * (int)sizeof(InT) + 48;
-  alignas(16) unsigned char stage[2][2 * RB][ROWB];
-  int offs[2][2 * RB];
-  uint64_t bar[2];
-  VT p[NV + 64];                  // P[u] = sum of columns < u, at word u + u / 32
+  static constexpr int NSTG = SSB_FUSED_STAGES;  // ring depth (row pairs in flight + 1)
+  alignas(16) unsigned char stage[NSTG][2 * RB][ROWB];
+  int offs[NSTG][2 * RB];
+  uint64_t bar[NSTG];
+  VT p[NV + 72];                  // P[u] = sum of columns < u, at word u + u / 32 (packed path: pp())
   VQ pq[SQ ? NV + 64 : 1];
 };
 
@@ -290,8 +379,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
   const char* base = reinterpret_cast<const char*>(in);
   const char* end_valid = base + ((g.R - 1) * g.in_ld + g.C) * ES;
   if (lane == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    for (int i = 0; i < SM::NSTG; ++i) mbar_init(&sm.bar[i], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -308,7 +396,8 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
     if (lane < 2 * RB) sm.offs[s][lane] = has ? sp.off : kNoRow;
     warp_issue(sp, has, dst, &sm.bar[s], lane);
   };
-  issue(0, 0);
+  for (int b = 0; b < SM::NSTG - 1; ++b)
+    if (b < nblk) issue(b, b);
 
   constexpr int NVR = PACK ? E / 2 : E;  // registers holding V
   VT V[NVR];
@@ -323,9 +412,9 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
   const int addr_b = lane + w + ((lane + w) >> 5);       // word of P[lane + w]
 
   for (int b = 0; b < nblk; ++b) {
-    const int s = b & 1;
-    if (b + 1 < nblk) issue(b + 1, s ^ 1);
-    mbar_wait(&sm.bar[s], (uint32_t)((b >> 1) & 1));
+    const int s = b % SM::NSTG;
+    if (b + SM::NSTG - 1 < nblk) issue(b + SM::NSTG - 1, (b + SM::NSTG - 1) % SM::NSTG);
+    mbar_wait(&sm.bar[s], (uint32_t)((b / SM::NSTG) & 1));
     const int64_t rb = r_beg + (int64_t)b * RB;
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
@@ -383,6 +472,12 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
       }
       if (r < r_beg + w - 1) continue;  // window not yet complete
       const int64_t i = r - (w - 1);
+      if constexpr (PACK) {
+        if (g.mask == ST_SUM) {  // uint8 sums: packed prefix + paired outputs
+          packed_sums_row<E>(V, sm.p, i * o.ld + oc0, reinterpret_cast<uint64_t*>(o.sum), nout, w, lane);
+          continue;
+        }
+      }
       // P[u] = sum_{c < u} V[c] at word u + u / 32; lane writes u = lane E + k + 1
       {
         auto vcol = [&](int k) -> VT {
@@ -425,7 +520,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
       if (!kFloat && !SQ && g.mask == ST_SUM) {
         uint64_t* dst = reinterpret_cast<uint64_t*>(o.sum) + obase;
         int a = addr_a, bw = addr_b;
-#pragma unroll 4
+#pragma unroll kFusedOutUnroll
         for (int qq = 0; qq < nq; ++qq, a += 33, bw += 33, dst += 32) {
           const VT sv = sub(sm.p[bw], sm.p[a]);
           if constexpr (sizeof(VT) == 4) st_cs(dst, (uint64_t)(uint32_t)sv);

@@ -159,4 +159,4 @@ def test_sweep_c5_band(sb, dev, hashes):
         sat, ld, outs = _engine.table_and_sweep(x, ElemKind.U8, v.shape[0], v.shape[1], 256, (StatKind.SUM,), dev,
                                                 onepass=onepass)
         assert digest(host(outs[StatKind.SUM], np.uint64)) == hashes[f"C5_sum_w256_rows{lo}_{hi}"]
-        assert bool(torch.equal(sat, sat2))
+        assert bool(torch.equal(sat[:, : v.shape[1] + 1], sat2[:, : v.shape[1] + 1]))
