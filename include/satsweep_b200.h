@@ -136,9 +136,12 @@ int ssb_sat_build_lookback(const void* in, int in_dtype, int64_t rows, int64_t c
  * stats SUM and/or MEAN; w <= 257 (u16: w <= 256).  ssb_sat_swa_supported
  * reports whether a request qualifies (1) or not (0); the workspace is
  * ssb_sat_swa_workspace_bytes.  ssb_sat_build_swa runs the faster pipeline
- * on B200 (table build, then the windows from the raster by the fused
- * kernel); ssb_sat_build_swa_onepass runs the one-pass kernel, whose table
- * writer also emits the windows (same results; A/B). */
+ * measured on B200: for uint8 (w <= 256) and uint16 (w <= 128) the table
+ * build and, concurrently on a forked stream joined back into `stream`, the
+ * windows from the raster by the fused kernel; otherwise the table build and
+ * the corner sweep.  ssb_sat_build_swa_onepass runs the one-pass kernel,
+ * whose table writer also emits the windows (same results; A/B, DESIGN.md
+ * section 4). */
 int ssb_sat_swa_supported(int in_dtype, int64_t w, int stat_mask);
 int64_t ssb_sat_swa_workspace_bytes(int in_dtype, int64_t rows, int64_t cols);
 /* Tiling of ssb_sat_build_swa: info4 = {warp strips, sweep segment height

@@ -409,6 +409,8 @@ cudaError_t launch_sat_build(int dtype, const void* in, int64_t R, int64_t C, in
                              cudaStream_t st);
 cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
                                 WinOut o, int* nonfinite, int nK, cudaStream_t st);
+cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_float, int in_dtype, int64_t R, int64_t C,
+                               int64_t sat_ld, int64_t w, int64_t s, int mask, WinOut o, cudaStream_t st);
 
 // Default: the table build (reduce-then-scan, sat_build.cu) and the fused
 // window kernel (window_fused.cu), which evaluates the windows from the
@@ -423,6 +425,14 @@ static bool swa_onepass_env() {
     return e && e[0] == 'o';
   }();
   return one;
+}
+
+// The fused kernel outruns the corner sweep for uint8 (w <= 256) and uint16
+// (w <= 128) rasters of at least 2^24 pixels (measured, scripts/pipe_probe.py,
+// scripts/bench_configs.py); elsewhere the table is read back by the corner
+// sweep (C2 int32: 0.74 vs 1.47 ms; C1 2048^2: launch-bound, 0.11 vs 0.17 ms).
+bool sweep_uses_fused(int dtype, int64_t R, int64_t C, int64_t w) {
+  return R * C >= ((int64_t)1 << 24) && ((dtype == IN_U8 && w <= 256) || (dtype == IN_U16 && w <= 128));
 }
 
 // Per-thread, per-device side stream and fork/join events (thread-local so
@@ -454,6 +464,11 @@ static cudaError_t side_stream(SideStream*& out) {
 cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld,
                              int64_t w, int mask, WinOut o, void* ws, cudaStream_t st, bool onepass) {
   if (!onepass && !swa_onepass_env()) {
+    if (!sweep_uses_fused(dtype, R, C, w)) {
+      cudaError_t e = launch_sat_build(dtype, in, R, C, in_ld, sat, nullptr, sat_ld, nullptr, nullptr, ws, nullptr, st);
+      if (e != cudaSuccess) return e;
+      return launch_window_eval(sat, nullptr, false, dtype, R, C, sat_ld, w, 1, mask, o, st);
+    }
     SideStream* side = nullptr;
     cudaError_t e = side_stream(side);
     if (e != cudaSuccess) return e;
