@@ -59,3 +59,26 @@ def test_validation_without_device(lib):
     assert rc == _lib.EINVAL
     with pytest.raises(_lib.InvalidWindowError):
         _lib.check(lib.ssb_window_eval(None, None, _lib.U8, 4, 4, 6, 0, 1, _lib.SUM, None, None, None, 1, None))
+
+
+def test_table_and_windows_contract(lib):
+    """ssb_sat_build_swa's request matrix (integer rasters, sum/mean, w <= 257, u16 sums in
+    32 bits) and its validation, all without a device."""
+    S = _lib.load().ssb_sat_swa_supported
+    assert S(_lib.U8, 1, _lib.SUM) == 1 and S(_lib.U8, 257, _lib.SUM | _lib.MEAN) == 1
+    assert S(_lib.U8, 258, _lib.SUM) == 0
+    assert S(_lib.U16, 256, _lib.SUM) == 1 and S(_lib.U16, 257, _lib.SUM) == 0
+    assert S(_lib.I32, 200, _lib.MEAN) == 1
+    assert S(_lib.F32, 10, _lib.SUM) == 0 and S(_lib.U8, 10, _lib.STD) == 0 and S(99, 10, _lib.SUM) == 0
+    assert lib.ssb_sat_swa_workspace_bytes(_lib.U8, 70000, 85000) >= lib.ssb_sat_workspace_bytes(_lib.U8, 70000,
+                                                                                                 85000, 0)
+    assert lib.ssb_sat_swa_workspace_bytes(_lib.F32, 10, 10) == -1
+    info = (ctypes.c_int64 * 4)()
+    assert lib.ssb_sat_swa_plan(_lib.U8, 70000, 85000, 256, info) == 0
+    nj_w, sr, nk, m = list(info)
+    assert nj_w * 1024 >= 85001 and sr * nk >= 70001 and m >= 1
+    for fn in (lib.ssb_sat_build_swa, lib.ssb_sat_build_swa_onepass):
+        rc = fn(None, _lib.F32, 8, 8, 8, None, 10, 3, _lib.SUM, None, None, 6, None, 0, None)
+        assert rc == _lib.EUNSUPPORTED
+        rc = fn(None, _lib.U8, 8, 8, 8, None, 10, 9, _lib.SUM, None, None, 6, None, 0, None)
+        assert rc == _lib.EINVAL and b"exceeds grid dims" in lib.ssb_last_error()
