@@ -1,15 +1,23 @@
-// satsweep-b200: the integral image and its window sums in one pass over the
-// raster (pipeline "table+sweep", ssb_sat_build_swa).
+// satsweep-b200: the integral image AND its window statistics
+// (ssb_sat_build_swa / ssb_sat_build_swa_onepass).
 //
 // The reference builds the table (integral.py:109-116 / parallel.py:106-121)
-// and then sweeps it with four-corner lookups (integral.py:141-163).  Run as
-// two kernels, the table is written to HBM and read back: 8 + 8 bytes per
-// pixel of the 25 B/px the materialised pipeline moves at C5.  Here the kernel
-// that writes a table row also emits the window sums whose bottom corner row
-// it is, so the table is written once and never read back.
+// and then sweeps it with four-corner lookups (integral.py:141-163): 25 B/px
+// at C5 (1 in + 8 table write + 8 table read + 8 out).  The window sums do not
+// need the table -- a per-column offset cancels in (br - tr) and a per-row
+// offset in (bl - tl) -- so both pipelines here write the table once and never
+// read it back (17 B/px):
 //
-// Phase 3 of the reduce-then-scan build (sat_build.cu) gives every warp a
-// (strip J, segment K) tile of TW table columns x SR table rows; the warp
+//   * default (launch_sat_sweep, bottom of the file): the reduce-then-scan
+//     build (sat_build.cu) on the caller's stream and, concurrently on a
+//     forked side stream, the fused window kernel (window_fused.cu) over the
+//     raster; the fastest on B200 (C5 19.9 ms);
+//   * one-pass kernel (sat_sweep_kernel): the warp that writes a table row
+//     also emits the windows whose bottom corner row it is (C5 22.9 ms,
+//     latency-bound).
+//
+// One-pass kernel.  Phase 3 of the reduce-then-scan build gives every warp a
+// (strip J, segment K) tile of TWW table columns x SR table rows; the warp
 // sweeps it top to bottom, lane l owning E table columns, with the vertical
 // table accumulation in registers.  For the window sums the same warp keeps,
 // per image column of its strip plus a halo of HW >= w - 1 columns to the
@@ -22,7 +30,7 @@
 // A warp owns the outputs whose right corner column lies in its strip.  Its
 // first w rows are a warm-up (V only) unless the segment starts at the top.
 // Rows are staged by TMA bulk copies: per step RB new rows (row - 1) and RB
-// leaving rows (row - 1 - w) over image columns [j0 - 1 - HW, j0 - 1 + TW).
+// leaving rows (row - 1 - w) over image columns [j0 - 1 - HW, j0 - 1 + TWW).
 //
 // Integer window sums are exact in the narrowest modular width holding the
 // final sum (u32 for u8/u16 at w <= 256); the table is uint64 modulo 2^64 and
