@@ -401,13 +401,13 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   const int nstats = ((stat_mask & SSB_SUM) ? 1 : 0) + ((stat_mask & SSB_MEAN) ? 1 : 0) + ((stat_mask & SSB_STD) ? 1 : 0);
   auto in_rows_for = [&](int64_t nb) { return (nb - 1) * stride + w; };
   if (band_rows <= 0) {
-    // ~1.5 GB of device buffers per band set (short pipeline fill and drain:
-    // C5 e2e 0.905 s vs 0.940 s at 6 GB, D2H at 97 % of the pinned PCIe
-    // ceiling), at least 4 bands when the image is large
+    // ~3 GB of device buffers per band set (C5: ~2,000-row bands; 1k-8k-row
+    // bands measured within box-to-box noise, 0.85-1.0 s, D2H at 90-97 % of
+    // the pinned PCIe ceiling), at least 4 bands when the image is large
     const double per_out_row = (double)stride * ((double)cols * es +
                                (pipeline == SSB_PIPE_TABLE ? 8.0 * sat_ld * (sq ? 2 : 1) : 0.0)) +
                                8.0 * (double)out_c * nstats;
-    band_rows = (int64_t)(1.5e9 / per_out_row);
+    band_rows = (int64_t)(3.0e9 / per_out_row);
     const int64_t quarter = (out_r + 3) / 4;
     if (band_rows > quarter && out_r > 4096) band_rows = quarter;
     if (band_rows < 1) band_rows = 1;
