@@ -160,3 +160,40 @@ def test_sweep_c5_band(sb, dev, hashes):
                                                 onepass=onepass)
         assert digest(host(outs[StatKind.SUM], np.uint64)) == hashes[f"C5_sum_w256_rows{lo}_{hi}"]
         assert bool(torch.equal(sat[:, : v.shape[1] + 1], sat2[:, : v.shape[1] + 1]))
+
+
+def test_sweep_concurrent_callers(sb, dev):
+    """ssb_sat_build_swa forks its window kernel onto a per-thread side stream:
+    threads calling it at once (each on its own torch stream, rasters >= 2^24 px so
+    the fork/join path runs) get correct, independent tables and sums."""
+    import threading
+
+    import torch
+
+    from paper_2410_16291_b200 import _engine
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    imgs = [raster("u8", 4200 + 16 * k, 4100, 40 + k) for k in range(3)]
+    refs = [O.swa(v, 64, "sum") for v in imgs]
+    tabs = [oracle_table(v)[-1] for v in imgs]  # last table row: the column totals
+    errs = []
+
+    def work(k):
+        try:
+            st = torch.cuda.Stream(dev)
+            with torch.cuda.stream(st):
+                x = to_dev(imgs[k], dev)
+                for _ in range(2):
+                    sat, _, outs = _engine.table_and_sweep(x, ElemKind.U8, *imgs[k].shape, 64, (StatKind.SUM,), dev)
+                    st.synchronize()
+                    np.testing.assert_array_equal(host(outs[StatKind.SUM], np.uint64), refs[k])
+                    np.testing.assert_array_equal(host(sat[-1, : imgs[k].shape[1] + 1], np.uint64), tabs[k])
+        except Exception as exc:  # pragma: no cover
+            errs.append(exc)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
