@@ -197,3 +197,28 @@ def test_sweep_concurrent_callers(sb, dev):
     for t in ts:
         t.join()
     assert not errs, errs
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_sweep_fork_join_fuzz(sb, dev, case):
+    """Seeded random rasters of >= 2^24 px (the fork/join path: table build on the
+    caller's stream, fused windows on the side stream) in every eligible kind and a
+    random window; table and sums vs the oracle."""
+    from paper_2410_16291_b200 import _engine
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    rng = np.random.default_rng(1000 + case)
+    kind = ["u8", "u8mask", "u16"][case % 3]
+    rows, cols = int(rng.integers(2100, 5200)), int(rng.integers(3300, 8200))
+    if rows * cols < 1 << 24:
+        cols = (1 << 24) // rows + 1
+    w = int(rng.integers(1, 129 if kind == "u16" else 257))
+    stats = [("sum",), ("mean",), ("sum", "mean")][int(rng.integers(0, 3))]
+    v = raster(kind, rows, cols, 2000 + case)
+    x = to_dev(v, dev)
+    sk = tuple(StatKind.parse(s) for s in stats)
+    sat, _, outs = _engine.table_and_sweep(x, ElemKind.from_dtype(v.dtype), rows, cols, w, sk, dev)
+    np.testing.assert_array_equal(host(sat[:, : cols + 1], np.uint64), oracle_table(v))
+    for s, k in zip(stats, sk):
+        np.testing.assert_array_equal(host(outs[k], np.float64 if s == "mean" else np.uint64), O.swa(v, w, s),
+                                      err_msg=f"{kind} {rows}x{cols} w={w} {s}")
