@@ -388,7 +388,11 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
     const int64_t rb = r_beg + (int64_t)b * RB;
     const int q = lane % RB;
     const bool old = lane >= RB;
+#ifdef SSB_FUSED_PROBE_OLD  // tuning probe: leaving rows read from the entering row (wrong sums; traffic as with an on-chip history)
+    const int64_t r = rb + q;
+#else
     const int64_t r = rb + q - (old ? w : 0);
+#endif
     const bool has = lane < 2 * RB && rb + q < r_end && (!old || rb + q - w >= r_beg);
     unsigned char* dst = sm.stage[s][lane < 2 * RB ? lane : 0];
     RowSpan sp;
