@@ -27,6 +27,11 @@ def build(st):
                                  ws.data_ptr(), ws.numel(), None, st.cuda_stream))
 
 
+def finish(st):  # phase 3 only, on carries left in the workspace by an earlier build (probe: a free reduce)
+    _lib.check(lib.ssb_sat_finish(x.data_ptr(), 0, rows, cols, cols, sat.data_ptr(), None, ld, None, None,
+                                  ws.data_ptr(), ws.numel(), st.cuda_stream))
+
+
 def fused(st):
     _lib.check(lib.ssb_window_fused(x.data_ptr(), 0, rows, cols, cols, w, 1, out.data_ptr(), None, None,
                                     cols - w + 1, None, int(os.environ.get("FSEG", 0)), st.cuda_stream))
@@ -68,4 +73,16 @@ def timeit(fn, n=10):
 print(f"sequential {timeit(seq):.3f} ms")
 print(f"concurrent build-first {timeit(lambda: conc(0)):.3f} ms")
 print(f"concurrent fused-first {timeit(lambda: conc(1)):.3f} ms")
+def conc_finish():
+    e = torch.cuda.Event()
+    e.record(sa)
+    sb_.wait_event(e)
+    finish(sa)
+    fused(sb_)
+    e2 = torch.cuda.Event()
+    e2.record(sb_)
+    sa.wait_event(e2)
+
+
+print(f"concurrent scan-only (probe: reduce + carries free) {timeit(conc_finish):.3f} ms")
 print(f"build alone {timeit(lambda: build(sa)):.3f} ms  fused alone {timeit(lambda: fused(sa)):.3f} ms")
