@@ -20,6 +20,9 @@
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
 
+#ifndef SSB_FUSED_PACK_E
+#define SSB_FUSED_PACK_E 2048  // uint8 packed strips: image columns per warp
+#endif
 #ifndef SSB_FUSED_STAGES
 #define SSB_FUSED_STAGES 2
 #endif
@@ -590,7 +593,10 @@ bool launch_strip(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* no
                   cudaError_t& err) {
   constexpr int E1 = 32 / (int)sizeof(InT);
   if constexpr (sizeof(InT) == 1 && sizeof(VT) == 4 && !SQ) {
-    if (g.w <= 256) { err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, true>(in, g, o, fi, nonfinite, nK, st); return true; }
+    if (g.w <= 256 && SSB_FUSED_PACK_E - 256 + 1 >= 64) {
+      err = launch_strip_t<InT, SSB_FUSED_PACK_E / 32, VT, VQ, SQ, true>(in, g, o, fi, nonfinite, nK, st);
+      return true;
+    }
   }
   if (32 * E1 - g.w + 1 < 64) return false;
   err = launch_strip_t<InT, E1, VT, VQ, SQ, false>(in, g, o, fi, nonfinite, nK, st);
