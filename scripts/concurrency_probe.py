@@ -19,7 +19,10 @@ sat = _device.empty((rows + 1, ld), np.uint64, dev, "t")
 out = _device.empty((rows - w + 1, cols - w + 1), np.uint64, dev, "o")
 ws = _device.empty((int(lib.ssb_sat_workspace_bytes(0, rows, cols, 0)),), np.uint8, dev, "ws")
 sa = torch.cuda.current_stream(dev)
-sb_ = torch.cuda.Stream(dev)
+sb_ = torch.cuda.Stream(dev, priority=int(os.environ.get("SIDE_PRIO", 0)))  # -1 = high priority
+if os.environ.get("MAIN_PRIO"):
+    sa = torch.cuda.Stream(dev, priority=int(os.environ["MAIN_PRIO"]))
+    torch.cuda.set_stream(sa)
 
 
 def build(st):
