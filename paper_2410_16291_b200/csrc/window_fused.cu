@@ -575,7 +575,12 @@ cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   g.sro = (g.out_r + nK - 1) / nK;
   nK = (g.out_r + g.sro - 1) / g.sro;
   auto kfn = fused_strip_kernel<InT, E, RB, VT, VQ, SQ, PACK>;
-  const size_t smem = sizeof(SM) * kStripWarps;
+  size_t smem = sizeof(SM) * kStripWarps;
+  {  // tuning: SSB_FUSED_SMEM_KB pads the CTA's shared memory to cap CTAs per SM
+     // (room for a concurrent kernel's CTAs on the same SMs)
+    static const long pad_kb = [] { const char* e = getenv("SSB_FUSED_SMEM_KB"); return e ? atol(e) : 0L; }();
+    if ((size_t)pad_kb * 1024 > smem) smem = (size_t)pad_kb * 1024;
+  }
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t warps = (int64_t)nJ * nK;
