@@ -60,6 +60,19 @@ __device__ __forceinline__ void warp_issue(const RowSpan& sp, bool has, unsigned
   if (has && sp.b > sp.a) bulk_g2s(dst_row + 16, sp.a, (uint32_t)(sp.b - sp.a), bar);
 }
 
+// warp_issue with an L2 cache policy on the bulk copies (createpolicy operand)
+__device__ __forceinline__ void warp_issue_hint(const RowSpan& sp, bool has, unsigned char* dst_row, uint64_t* bar,
+                                                int lane, uint64_t pol) {
+  uint32_t bytes = (has && sp.b > sp.a) ? (uint32_t)(sp.b - sp.a) : 0u;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, d);
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+  __syncwarp();
+  if (has && sp.b > sp.a) bulk_g2s_hint(dst_row + 16, sp.a, (uint32_t)(sp.b - sp.a), bar, pol);
+}
+
 template <int NO, int SW>
 __device__ __forceinline__ void shift_words(const uint32_t* w, uint32_t* o, int sb) {
 #pragma unroll

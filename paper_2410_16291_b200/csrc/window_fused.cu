@@ -20,6 +20,9 @@
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
 
+#ifndef SSB_FUSED_LOAD_HINT
+#define SSB_FUSED_LOAD_HINT 0
+#endif
 #ifndef SSB_FUSED_PACK_E
 #define SSB_FUSED_PACK_E 2048  // uint8 packed strips: image columns per warp
 #endif
@@ -401,7 +404,13 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
     RowSpan sp;
     if (has) sp = row_span(base + r * g.in_ld * ES, c_lo, c_hi, ES, end_valid, dst);
     if (lane < 2 * RB) sm.offs[s][lane] = has ? sp.off : kNoRow;
+#if SSB_FUSED_LOAD_HINT == 1  // tuning: raster rows streamed with evict-first / evict-last L2 policies
+    warp_issue_hint(sp, has, dst, &sm.bar[s], lane, policy_evict_first());
+#elif SSB_FUSED_LOAD_HINT == 2
+    warp_issue_hint(sp, has, dst, &sm.bar[s], lane, old ? policy_evict_first() : policy_evict_last());
+#else
     warp_issue(sp, has, dst, &sm.bar[s], lane);
+#endif
   };
   for (int b = 0; b < SM::NSTG - 1; ++b)
     if (b < nblk) issue(b, b);
