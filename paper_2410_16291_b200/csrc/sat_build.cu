@@ -42,6 +42,9 @@
 #ifndef SSB_SCAN_STAGES
 #define SSB_SCAN_STAGES 2
 #endif
+#ifndef SSB_SCAN_RB
+#define SSB_SCAN_RB 0  // rows per TMA stage in the scan (0: 8 for 1-byte, 4 for wider pixels)
+#endif
 #ifndef SSB_SCAN_MINB_SQ
 #define SSB_SCAN_MINB_SQ 2
 #endif
@@ -378,7 +381,7 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
   using LocSq = typename Tr::LocSq;
   using Acc = typename Tr::Acc;
   using G = Geo<InT>;
-  using WS = WarpStage<InT, 0, SSB_SCAN_STAGES>;
+  using WS = WarpStage<InT, SSB_SCAN_RB, SSB_SCAN_STAGES>;
   constexpr int TW = G::TW, E = G::E, RB = WS::RBW, NSTG = WS::NSTG;
   static_assert(E % 4 == 0, "256-bit stores");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -549,7 +552,7 @@ cudaError_t launch_sat_finish_t(const void* in, int64_t R, int64_t C, int64_t in
   if (carry) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp, reinterpret_cast<const Acc*>(carry), p.nK, p.PC); note_launch(1); }
   if (SQ && carry_sq) { sat_apply_carry_kernel<Acc><<<nb_cols, kThreads, 0, st>>>(colp_sq, reinterpret_cast<const Acc*>(carry_sq), p.nK, p.PC); note_launch(1); }
   const int tb = (int)(((int64_t)p.nJ * p.nK + kScanWarps - 1) / kScanWarps);
-  const int smem = (int)(sizeof(WarpStage<InT, 0, SSB_SCAN_STAGES>) * kScanWarps);
+  const int smem = (int)(sizeof(WarpStage<InT, SSB_SCAN_RB, SSB_SCAN_STAGES>) * kScanWarps);
   cudaError_t e = cudaFuncSetAttribute(sat_scan_kernel<InT, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   sat_scan_kernel<InT, SQ><<<tb, 32 * kScanWarps, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
