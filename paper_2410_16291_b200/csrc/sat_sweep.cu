@@ -86,7 +86,7 @@ struct SweepSmem {
   alignas(16) unsigned char stage[2][2 * RB][SG::ROWB];
   int offs[2][2 * RB];
   uint64_t bar[2];
-  VT p[SG::NV + SG::NV / 32 + 2];  // P[u] = sum_{v < u} V[v] at word u + u / 32
+  VT p[SG::NV + SG::NV / 32 + 8];  // P[u] = sum_{v < u} V[v] at word u + u / 32 (packed path: pp(u + d))
 };
 
 // V +/-= one staged row's elements (NW packed words per lane).  Packed (uint8):
@@ -108,6 +108,92 @@ __device__ __forceinline__ void vupdate(VT (&V)[NV], const uint32_t (&x)[NW]) {
       V[k] = ADD ? add(V[k], v) : sub(V[k], v);
     }
   }
+}
+
+__device__ __forceinline__ unsigned long long get4(const U64x4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void set4(U64x4& v, int i, unsigned long long x) {
+  if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
+}
+
+// word index of P entry v: two pad words per 64 keep even v 8-byte aligned
+__device__ __forceinline__ int opp(int v) { return v + 2 * (v >> 6); }
+
+// One output row of the one-pass kernel for uint8 sums from packed vertical
+// sums (Vh: the lane's EH halo columns, Vm: its E strip columns; V[2g] holds
+// columns 4g, 4g+2 and V[2g+1] columns 4g+1, 4g+3 as 16-bit halves).  P index
+// u (halo u = lane EH + k + 1, strip u = HW + lane E + k + 1) is stored at word
+// opp(u + d), d chosen so that every output pair (j, j+1) that is 16-byte
+// aligned in global memory reads its operands with 64-bit shared loads; the
+// running prefix takes one DP2A per column.  orow = output of column j_lo,
+// u0 = its P index.
+template <int E, int EH, int HW>
+__device__ __forceinline__ void onepass_packed_row(const uint32_t (&Vm)[E / 2], const uint32_t (&Vh)[EH / 2],
+                                                   uint32_t* P, uint64_t* __restrict__ orow, int u0, int nout, int w,
+                                                   int lane) {
+  const int e = (int)((reinterpret_cast<uintptr_t>(orow) >> 3) & 1);  // first output not 16-byte aligned
+  const int d = (u0 + e) & 1;
+  uint32_t th = 0u, tm = 0u;
+#pragma unroll
+  for (int i = 0; i < EH / 2; ++i) th = __dp2a_lo(Vh[i], 0x0101u, th);
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i) tm = __dp2a_lo(Vm[i], 0x0101u, tm);
+  const uint32_t ih = warp_incl_scan(th, lane);
+  const uint32_t hall = __shfl_sync(0xffffffffu, ih, 31);
+  const uint32_t im = warp_incl_scan(tm, lane);
+  auto write4 = [&](const uint32_t (&V)[2], uint32_t& run, int u) {
+    const uint32_t r0 = __dp2a_lo(V[0], 0x0001u, run);
+    const uint32_t r1 = __dp2a_lo(V[1], 0x0001u, r0);
+    const uint32_t r2 = __dp2a_lo(V[0], 0x0100u, r1);
+    const uint32_t r3 = __dp2a_lo(V[1], 0x0100u, r2);
+    P[opp(u + d)] = r0;
+    P[opp(u + 1 + d)] = r1;
+    P[opp(u + 2 + d)] = r2;
+    P[opp(u + 3 + d)] = r3;
+    run = r3;
+  };
+  uint32_t run = ih - th;
+#pragma unroll
+  for (int q = 0; q < EH / 4; ++q) {
+    const uint32_t v2[2] = {Vh[2 * q], Vh[2 * q + 1]};
+    write4(v2, run, lane * EH + 4 * q + 1);
+  }
+  run = hall + (im - tm);
+#pragma unroll
+  for (int q = 0; q < E / 4; ++q) {
+    const uint32_t v2[2] = {Vm[2 * q], Vm[2 * q + 1]};
+    write4(v2, run, HW + lane * E + 4 * q + 1);
+  }
+  if (lane == 0) P[opp(d)] = 0u;
+  __syncwarp();
+  if (lane == 0) {
+    if (e) orow[0] = (uint64_t)(P[opp(u0 + w + d)] - P[opp(u0 + d)]);
+    if ((nout - e) & 1) orow[nout - 1] = (uint64_t)(P[opp(u0 + nout - 1 + w + d)] - P[opp(u0 + nout - 1 + d)]);
+  }
+  const int npair = (nout - e) >> 1;
+  const int va = u0 + e + d + 2 * lane;  // even
+  const uint32_t* pa = P + opp(va);
+  uint64_t* dst = orow + e + 2 * lane;
+  const int nq = (npair - lane + 31) >> 5;
+  if ((w & 1) == 0) {
+    const uint32_t* pb = P + opp(va + w);
+#pragma unroll 4
+    for (int qq = 0; qq < nq; ++qq) {
+      const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
+      const uint2 B = *reinterpret_cast<const uint2*>(pb + 66 * qq);
+      st_cs2(dst + 64 * qq, (uint64_t)(B.x - A.x), (uint64_t)(B.y - A.y));
+    }
+  } else {
+    const uint32_t* pb0 = P + opp(va + w);
+    const uint32_t* pb1 = P + opp(va + w + 1);
+#pragma unroll 4
+    for (int qq = 0; qq < nq; ++qq) {
+      const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
+      st_cs2(dst + 64 * qq, (uint64_t)(pb0[66 * qq] - A.x), (uint64_t)(pb1[66 * qq] - A.y));
+    }
+  }
+  __syncwarp();  // P is rewritten by the next row
 }
 
 // sum of a lane's E elements in the table's local type
@@ -200,9 +286,12 @@ sat_sweep_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld
   };
   issue(0, 0);
 
-  Acc acc[E];
+  // table accumulators as 4-element vectors: one 256-bit store each without
+  // register re-packing (a plain Acc[E] array cost 8 moves per store)
+  U64x4 acc4[E / 4];
 #pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = cbase + k < PC ? top[(int64_t)K * top_stride + cbase + k] : Acc(0);
+  for (int k = 0; k < E; ++k)
+    set4(acc4[k / 4], k % 4, (unsigned long long)(cbase + k < PC ? top[(int64_t)K * top_stride + cbase + k] : Acc(0)));
   constexpr int NVM = PACK ? E / 2 : E, NVH = PACK ? EH / 2 : EH;
   VT Vm[NVM], Vh[NVH];
 #pragma unroll
@@ -249,16 +338,47 @@ sat_sweep_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld
       if (row < k0) continue;  // warm-up row
       {  // table row: strip-local prefix + left carry, accumulated down the column
         const Loc t = lane_sum<InT, E>(xm);
-        Loc run = sub(warp_incl_scan(t, lane), t);
-        const Acc left = __shfl_sync(0xffffffffu, rlv, q);
+        // element k's row value = left carry + lanes to the left + lane-local prefix
+        const Acc base = add(__shfl_sync(0xffffffffu, rlv, q), (Acc)sub(warp_incl_scan(t, lane), t));
+        if constexpr (sizeof(InT) == 1) {
+          // lane-local prefix by DP4A: bytes 0..m of word i in one step from the group base
+          uint32_t g = 0u;
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          run = add(run, conv<Loc>(elem<InT>(xm, k)));
-          acc[k] = add(acc[k], add(left, (Acc)run));
+          for (int i = 0; i < NWM; ++i) {
+            const uint32_t p0 = __dp4a(xm[i], 0x00000001u, g), p1 = __dp4a(xm[i], 0x00000101u, g);
+            const uint32_t p2 = __dp4a(xm[i], 0x00010101u, g), p3 = __dp4a(xm[i], 0x01010101u, g);
+            acc4[i].x += base + p0;
+            acc4[i].y += base + p1;
+            acc4[i].z += base + p2;
+            acc4[i].w += base + p3;
+            g = p3;
+          }
+        } else {
+          Loc pre = Loc(0);
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            pre = add(pre, conv<Loc>(elem<InT>(xm, k)));
+            set4(acc4[k / 4], k % 4, get4(acc4[k / 4], k % 4) + (unsigned long long)add(base, (Acc)pre));
+          }
         }
-        store_lane_cols<Acc, E>(sat + row * sat_ld + cbase, acc, cbase, PC);
+        Acc* dst = sat + row * sat_ld + cbase;
+        if (cbase + E <= PC) {
+#pragma unroll
+          for (int i = 0; i < E / 4; ++i) st256(dst + 4 * i, acc4[i]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (cbase + k < PC) st_cs(dst + k, (Acc)get4(acc4[k / 4], k % 4));
+        }
       }
       if (row < w || nout <= 0) continue;  // no window ends on this row
+      if constexpr (PACK) {
+        if (mask == ST_SUM) {  // uint8 sums: DP2A prefix, paired 16-byte output stores
+          onepass_packed_row<E, EH, HW>(Vm, Vh, sm.p, reinterpret_cast<uint64_t*>(o.sum) + (row - w) * o.ld + j_lo,
+                                       (int)(j_lo - cb), nout, w, lane);
+          continue;
+        }
+      }
       {  // P = prefix of V over [halo | strip]
         VT th = VT(0), tm = VT(0);
 #pragma unroll
