@@ -222,3 +222,16 @@ def test_sweep_fork_join_fuzz(sb, dev, case):
     for s, k in zip(stats, sk):
         np.testing.assert_array_equal(host(outs[k], np.float64 if s == "mean" else np.uint64), O.swa(v, w, s),
                                       err_msg=f"{kind} {rows}x{cols} w={w} {s}")
+
+
+def test_sweep_host_bands(sb):
+    """numpy in, numpy out (ssb_swa_host): bands of >= 2^24 px take the table + concurrent
+    fused-windows path inside the banded H2D/compute/D2H pipeline; sums and means equal the
+    oracle's, and the caller's array is untouched."""
+    v = raster("u8", 9000, 9000, 77)
+    before = v.copy()
+    got = sb.swa_stats(v, 256, ("sum", "mean"), pipeline="table")
+    assert got["sum"].dtype == np.uint64 and got["mean"].dtype == np.float64
+    np.testing.assert_array_equal(got["sum"], O.swa(v, 256, "sum"))
+    np.testing.assert_array_equal(got["mean"], O.swa(v, 256, "mean"))
+    np.testing.assert_array_equal(v, before)
