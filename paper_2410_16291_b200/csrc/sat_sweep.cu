@@ -47,6 +47,9 @@
 #ifndef SSB_SWEEP_SPW_U8
 #define SSB_SWEEP_SPW_U8 2  // uint8: build strips (512 table columns) per warp
 #endif
+#ifndef SSB_SWEEP_RB_U8
+#define SSB_SWEEP_RB_U8 2  // uint8: rows staged per TMA step (new + leaving rows each)
+#endif
 #ifndef SSB_SWEEP_WPC
 #define SSB_SWEEP_WPC 4
 #endif
@@ -66,7 +69,7 @@ template <typename InT> struct SweepCfg;
 // SPW = build strips per warp (the warp's table columns TWW = SPW * TW),
 // RB = rows staged per step, VT = modular type of the vertical sums,
 // PACK = two 16-bit vertical sums per register (uint8, w <= 257)
-template <> struct SweepCfg<uint8_t> { static constexpr int SPW = SSB_SWEEP_SPW_U8, RB = 2; using VT = uint32_t; static constexpr bool PACK = true; };
+template <> struct SweepCfg<uint8_t> { static constexpr int SPW = SSB_SWEEP_SPW_U8, RB = SSB_SWEEP_RB_U8; using VT = uint32_t; static constexpr bool PACK = true; };
 template <> struct SweepCfg<uint16_t> { static constexpr int SPW = 1, RB = 2; using VT = uint32_t; static constexpr bool PACK = false; };
 template <> struct SweepCfg<int32_t> { static constexpr int SPW = 1, RB = 2; using VT = uint64_t; static constexpr bool PACK = false; };
 
