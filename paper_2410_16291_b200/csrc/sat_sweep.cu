@@ -48,7 +48,10 @@
 #define SSB_SWEEP_SPW_U8 2  // uint8: build strips (512 table columns) per warp
 #endif
 #ifndef SSB_SWEEP_RB_U8
-#define SSB_SWEEP_RB_U8 2  // uint8: rows staged per TMA step (new + leaving rows each)
+#define SSB_SWEEP_RB_U8 1  // uint8: rows staged per TMA step (new + leaving rows each)
+#endif
+#ifndef SSB_SWEEP_STAGES_U8
+#define SSB_SWEEP_STAGES_U8 6  // uint8: TMA ring depth (6 x 1 row measured 1.5 % faster than 2 x 2 at C5)
 #endif
 #ifndef SSB_SWEEP_WPC
 #define SSB_SWEEP_WPC 4
@@ -67,11 +70,23 @@ constexpr int kSweepHalo = 256;  // halo columns: windows up to 257
 
 template <typename InT> struct SweepCfg;
 // SPW = build strips per warp (the warp's table columns TWW = SPW * TW),
-// RB = rows staged per step, VT = modular type of the vertical sums,
+// RB = rows staged per step, NST = TMA ring depth, VT = modular type of the vertical sums,
 // PACK = two 16-bit vertical sums per register (uint8, w <= 257)
-template <> struct SweepCfg<uint8_t> { static constexpr int SPW = SSB_SWEEP_SPW_U8, RB = SSB_SWEEP_RB_U8; using VT = uint32_t; static constexpr bool PACK = true; };
-template <> struct SweepCfg<uint16_t> { static constexpr int SPW = 1, RB = 2; using VT = uint32_t; static constexpr bool PACK = false; };
-template <> struct SweepCfg<int32_t> { static constexpr int SPW = 1, RB = 2; using VT = uint64_t; static constexpr bool PACK = false; };
+template <> struct SweepCfg<uint8_t> {
+  static constexpr int SPW = SSB_SWEEP_SPW_U8, RB = SSB_SWEEP_RB_U8, NST = SSB_SWEEP_STAGES_U8;
+  using VT = uint32_t;
+  static constexpr bool PACK = true;
+};
+template <> struct SweepCfg<uint16_t> {
+  static constexpr int SPW = 1, RB = 2, NST = 2;
+  using VT = uint32_t;
+  static constexpr bool PACK = false;
+};
+template <> struct SweepCfg<int32_t> {
+  static constexpr int SPW = 1, RB = 2, NST = 2;
+  using VT = uint64_t;
+  static constexpr bool PACK = false;
+};
 
 template <typename InT, int HW>
 struct SweepGeo {
@@ -89,9 +104,10 @@ struct SweepSmem {
   using SG = SweepGeo<InT, HW>;
   static constexpr int RB = Cfg::RB;
   alignas(16) unsigned char guard[64];  // a halo lane left of column 0 may read a few bytes before its row
-  alignas(16) unsigned char stage[2][2 * RB][SG::ROWB];
-  int offs[2][2 * RB];
-  uint64_t bar[2];
+  static constexpr int NST = Cfg::NST;  // TMA ring depth
+  alignas(16) unsigned char stage[NST][2 * RB][SG::ROWB];
+  int offs[NST][2 * RB];
+  uint64_t bar[NST];
   VT p[SG::NV + SG::NV / 32 + 8];  // P[u] = sum_{v < u} V[v] at word u + u / 32 (packed path: pp(u + d))
 };
 
@@ -271,8 +287,7 @@ sat_sweep_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld
   const int nout = (int)(j_hi - j_lo);
 
   if (lane == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    for (int i = 0; i < SM::NST; ++i) mbar_init(&sm.bar[i], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -290,7 +305,8 @@ sat_sweep_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld
     if (lane < 2 * RB) sm.offs[s][lane] = has ? sp.off : kNoRow;
     warp_issue(sp, has, dst, &sm.bar[s], lane);
   };
-  issue(0, 0);
+  for (int b = 0; b < SM::NST - 1; ++b)
+    if (b < nblk) issue(b, b);
 
   // table accumulators as 4-element vectors: one 256-bit store each without
   // register re-packing (a plain Acc[E] array cost 8 moves per store)
@@ -320,12 +336,12 @@ sat_sweep_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld
     }
   };
   for (int b = 0; b < nblk; ++b) {
-    const int s = b & 1;
-    if (b + 1 < nblk) issue(b + 1, s ^ 1);
+    const int s = b % SM::NST;
+    if (b + SM::NST - 1 < nblk) issue(b + SM::NST - 1, (b + SM::NST - 1) % SM::NST);
     const int64_t rb = ra + (int64_t)b * RB;
     Acc rlv = Acc(0);  // lane q: left carry of table row rb + q
     if (lane < RB && rb + lane >= k0 && rb + lane < k1) rlv = rl[(rb + lane) * nJ + J * SPW];
-    mbar_wait(&sm.bar[s], (uint32_t)((b >> 1) & 1));
+    mbar_wait(&sm.bar[s], (uint32_t)((b / SM::NST) & 1));
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
       const int64_t row = rb + q;
