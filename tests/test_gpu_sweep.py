@@ -235,3 +235,30 @@ def test_sweep_host_bands(sb):
     np.testing.assert_array_equal(got["sum"], O.swa(v, 256, "sum"))
     np.testing.assert_array_equal(got["mean"], O.swa(v, 256, "mean"))
     np.testing.assert_array_equal(v, before)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_onepass_fuzz(sb, dev, case):
+    """Seeded random shapes, kinds, windows and stats through the one-pass kernel
+    (ssb_sat_build_swa_onepass): strips partly outside the image, segments with and
+    without warm-up, odd and even windows, unaligned output rows; table and windows
+    vs the oracle."""
+    from paper_2410_16291_b200 import _engine
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    rng = np.random.default_rng(5000 + case)
+    kind = ["u8", "u8mask", "u16", "i32"][case % 4]
+    rows, cols = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+    if case >= 10:  # a couple of large ones: one-wave tiling, long segments
+        rows, cols = int(rng.integers(5000, 9000)), int(rng.integers(3000, 6000))
+    wmax = min(rows, cols, 256 if kind == "u16" else 257)
+    w = int(rng.integers(1, wmax + 1))
+    stats = [("sum",), ("mean",), ("sum", "mean")][int(rng.integers(0, 3))]
+    v = raster(kind, rows, cols, 6000 + case)
+    x = to_dev(v, dev)
+    sk = tuple(StatKind.parse(s) for s in stats)
+    sat, _, outs = _engine.table_and_sweep(x, ElemKind.from_dtype(v.dtype), rows, cols, w, sk, dev, onepass=True)
+    np.testing.assert_array_equal(host(sat[:, : cols + 1], np.uint64), oracle_table(v))
+    for s, k in zip(stats, sk):
+        dt = np.float64 if s == "mean" else (np.int64 if kind == "i32" else np.uint64)
+        np.testing.assert_array_equal(host(outs[k], dt), O.swa(v, w, s), err_msg=f"{kind} {rows}x{cols} w={w} {s}")
