@@ -27,15 +27,18 @@
  *
  * Conventions
  *   - Device rasters must be 16-byte aligned (rows are staged with TMA bulk
- *     copies); tables 16-byte aligned with an even pitch.
+ *     copies).  Tables that the library WRITES must be 32-byte aligned with
+ *     a pitch that is a multiple of 4 elements (rows are stored with 256-bit
+ *     stores; SSB_EINVAL otherwise); tables it only READS need 16-byte
+ *     alignment and an even pitch for the TMA corner sweep.
  *   - Every device pointer is caller-allocated device memory; the library keeps
  *     no persistent allocations (ssb_swa_host allocates and frees its own
  *     staging per call).
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device entry
  *     points are asynchronous on that stream.
  *   - Tables are (rows+1) x (cols+1) with a zero border row/column and row
- *     pitch `sat_ld` elements; `sat_ld` must be even and the table 16-byte
- *     aligned.  Integer tables are uint64 modulo 2^64, float tables double.
+ *     pitch `sat_ld` elements (see the alignment rule above).  Integer
+ *     tables are uint64 modulo 2^64, float tables double.
  *   - Returns SSB_OK or an error code; ssb_last_error() gives a thread-local
  *     message.  No entry point falls back to a CPU implementation.
  */

@@ -63,20 +63,24 @@ def new_flag(device):
 
 
 class _Scratch(threading.local):
-    """Grow-only per-thread, per-device scratch buffers for tables that never
-    leave the library (swa / multi_window), so repeated calls do not churn
-    multi-GB allocations through the caching allocator.  Thread-local, so
-    concurrent callers never share a buffer.  release_scratch() frees them."""
+    """Grow-only scratch buffers for tables that never leave the library
+    (swa / multi_window), so repeated calls do not churn multi-GB allocations
+    through the caching allocator.  Keyed by thread, device AND stream: every
+    kernel touching a buffer runs on the stream it was allocated for, so a call
+    on another stream can never overwrite a table or workspace that an earlier
+    call's kernels are still reading, and growing a buffer frees the old one in
+    that stream's order.  release_scratch() frees them."""
 
     def __init__(self):
         self.bufs = {}
 
     def get(self, key, nbytes: int, device):
-        cur = self.bufs.get((key, str(device)))
+        k = (key, str(device), _device.stream_ptr(device))
+        cur = self.bufs.get(k)
         if cur is None or cur.numel() < nbytes:
-            self.bufs.pop((key, str(device)), None)
+            self.bufs.pop(k, None)
             cur = _device.empty((max(nbytes, 8),), np.uint8, device, f"{nbytes} bytes of scratch")
-            self.bufs[(key, str(device))] = cur
+            self.bufs[k] = cur
         return cur
 
     def clear(self):
@@ -214,6 +218,32 @@ def choose_pipeline(pipeline: str, kind: ElemKind, w: int, stride: int) -> str:
 
 def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None):
     """All requested stats for one window on the device; returns {StatKind: tensor}."""
+    with on_device(img):
+        return _run_device(img, w, stride, stats, pipeline, outs)
+
+
+def on_device(img: ImageGrid):
+    """Make the raster's device current (streams, scratch and allocations follow it)."""
+    import contextlib
+
+    if img.on_device:
+        return _device.torch().cuda.device(img.values.device)
+    return contextlib.nullcontext()
+
+
+def device_scoped(fn):
+    """Decorator: run ``fn(img, ...)`` with the raster's device current."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(img, *args, **kwargs):
+        with on_device(img):
+            return fn(img, *args, **kwargs)
+
+    return wrapper
+
+
+def _run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str, outs):
     x, dev = device_input(img)
     rows, cols = img.rows, img.cols
     pipe = choose_pipeline(pipeline, img.elem_kind, w, stride)

@@ -8,7 +8,9 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -82,6 +84,18 @@ int check_image(int dtype, int64_t rows, int64_t cols, int64_t in_ld) {
   return SSB_OK;
 }
 
+// Table writers store rows with 256-bit st.global.v4.b64 (sat_tiles.cuh,
+// sat_sweep.cu), so every table row must start on a 32-byte boundary: the
+// table base 32-byte aligned and the pitch a multiple of 4 elements.
+int check_table_out(const void* sat, const void* sat_sq, int64_t sat_ld, int64_t cols) {
+  if (sat_ld < cols + 1 || (sat_ld & 3))
+    return fail(SSB_EINVAL, "sat_ld must be a multiple of 4 and >= cols+1 (got %lld for %lld cols)", (long long)sat_ld,
+                (long long)cols);
+  if ((reinterpret_cast<uintptr_t>(sat) & 31) || (reinterpret_cast<uintptr_t>(sat_sq) & 31))
+    return fail(SSB_EINVAL, "tables must be 32-byte aligned");
+  return SSB_OK;
+}
+
 int check_aligned(const void* p, const char* what) {
   if (reinterpret_cast<uintptr_t>(p) & 15) return fail(SSB_EINVAL, "%s must be 16-byte aligned", what);
   return SSB_OK;
@@ -104,6 +118,27 @@ int check_stats(int dtype, int mask) {
 }
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Launches go to the caller's stream, which may belong to a device other than
+// the calling thread's current one: make the stream's device current for the
+// call and restore the caller's device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(void* stream) {
+    int d = 0;
+    if ((err = cudaStreamGetDevice(as_stream(stream), &d)) != cudaSuccess) return;
+    if ((err = cudaGetDevice(&prev)) != cudaSuccess) return;
+    if (d != prev) err = cudaSetDevice(d);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define SSB_DEVICE_GUARD(stream)                                  \
+  DeviceGuard device_guard_(stream);                              \
+  if (device_guard_.err != cudaSuccess) return cuda_fail(device_guard_.err, "stream device")
 }  // namespace
 
 // io.cu reports through the same thread-local message
@@ -149,6 +184,7 @@ int ssb_sat_prepare(const void* in, int in_dtype, int64_t rows, int64_t cols, in
   if ((rc = check_aligned(in, "input raster"))) return rc;
   const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, with_squares != 0);
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_sat_prepare(in_dtype, in, rows, cols, in_ld, with_squares != 0, ws, band_totals,
                                      band_totals_sq, nonfinite_flag, as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_prepare");
@@ -160,11 +196,10 @@ int ssb_sat_finish(const void* in, int in_dtype, int64_t rows, int64_t cols, int
   if (rc) return rc;
   if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
   if ((rc = check_aligned(in, "input raster"))) return rc;
-  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
-  if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
-    return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  if ((rc = check_table_out(sat, sat_sq, sat_ld, cols))) return rc;
   const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, sat_sq != nullptr);
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_sat_finish(in_dtype, in, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws,
                                     as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_finish");
@@ -178,11 +213,10 @@ int ssb_sat_build(const void* in, int in_dtype, int64_t rows, int64_t cols, int6
   if (in_dtype == SSB_I32 && sat_sq) return fail(SSB_EUNSUPPORTED, "squared tables are not supported for int32 input");
   if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
   if ((rc = check_aligned(in, "input raster"))) return rc;
-  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
-  if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
-    return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  if ((rc = check_table_out(sat, sat_sq, sat_ld, cols))) return rc;
   const int64_t need = sat_workspace_bytes(in_dtype, rows, cols, sat_sq != nullptr);
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_sat_build(in_dtype, in, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws,
                                    nonfinite_flag, as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build");
@@ -197,11 +231,10 @@ int ssb_sat_build_lookback(const void* in, int in_dtype, int64_t rows, int64_t c
     return fail(SSB_EUNSUPPORTED, "the single-pass build takes integer input (no squares for int32)");
   if (!sat && !sat_sq) return fail(SSB_EINVAL, "no table to write");
   if ((rc = check_aligned(in, "input raster"))) return rc;
-  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
-  if ((reinterpret_cast<uintptr_t>(sat) & 15) || (sat_sq && (reinterpret_cast<uintptr_t>(sat_sq) & 15)))
-    return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  if ((rc = check_table_out(sat, sat_sq, sat_ld, cols))) return rc;
   const int64_t need = sat_onepass_workspace_bytes(in_dtype, rows, cols, sat_sq != nullptr);
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_sat_onepass(in_dtype, in, rows, cols, in_ld, sat, sat_sq, sat_ld, carry, carry_sq, ws,
                                      as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build_lookback");
@@ -221,6 +254,7 @@ int ssb_window_eval(const void* sat, const void* sat_sq, int in_dtype, int64_t r
   const int64_t out_c = (cols - w) / stride + 1;
   if (out_ld < out_c) return fail(SSB_EINVAL, "out_ld < output cols");
   WinOut o{out_sum, out_mean, out_std, out_ld};
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_window_eval(sat, sat_sq, in_dtype == SSB_F32, in_dtype, rows, cols, sat_ld, w, stride,
                                      stat_mask, o, as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_window_eval");
@@ -256,18 +290,51 @@ static int sat_build_swa_impl(bool onepass, const void* in, int in_dtype, int64_
                 in_dtype, (long long)w);
   if ((rc = check_aligned(in, "input raster"))) return rc;
   if (!sat) return fail(SSB_EINVAL, "no table to write");
-  if (sat_ld < cols + 1 || (sat_ld & 1)) return fail(SSB_EINVAL, "sat_ld must be even and >= cols+1");
-  if (reinterpret_cast<uintptr_t>(sat) & 15) return fail(SSB_EINVAL, "tables must be 16-byte aligned");
+  if ((rc = check_table_out(sat, nullptr, sat_ld, cols))) return rc;
   if (((stat_mask & SSB_SUM) && !out_sum) || ((stat_mask & SSB_MEAN) && !out_mean))
     return fail(SSB_EINVAL, "missing output buffer");
   if (out_ld < cols - w + 1) return fail(SSB_EINVAL, "out_ld < output cols");
   const int64_t need = sat_sweep_workspace_bytes(in_dtype, rows, cols);
   if (!ws || ws_bytes < need) return fail(SSB_EINVAL, "workspace too small: need %lld bytes", (long long)need);
   WinOut o{out_sum, out_mean, nullptr, out_ld};
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_sat_sweep(in_dtype, in, rows, cols, in_ld, sat, sat_ld, w, stat_mask, o, ws,
                                    as_stream(stream), onepass);
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sat_build_swa");
 }
+
+namespace {
+// buffer sets in flight for ssb_swa_host (SSB_HOST_SETS overrides; read once)
+int host_sets() {
+  static const int n = [] {
+    const char* e = getenv("SSB_HOST_SETS");
+    const int v = e ? atoi(e) : 3;
+    return v < 1 ? 1 : v > 8 ? 8 : v;
+  }();
+  return n;
+}
+
+// one private pool per device for ssb_swa_host, created on first use (the
+// pool object holds no memory between calls: every call trims it to zero)
+cudaError_t host_pool(int device, cudaMemPool_t* out) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaError_t e = cudaMemPoolCreate(&pools[device], &props);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;  // keep blocks for reuse across the bands of one call
+    cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = pools[device];
+  return cudaSuccess;
+}
+}  // namespace
 
 extern "C" {
 
@@ -298,6 +365,7 @@ int ssb_window_eval_multi(const void* sat, const void* sat_sq, int in_dtype, int
   if (rc) return rc;
   if (!sat || sat_ld < cols + 1) return fail(SSB_EINVAL, "bad table");
   if ((stat_mask & SSB_STD) && !sat_sq) return fail(SSB_EINVAL, "squared sums required for std dev");
+  SSB_DEVICE_GUARD(stream);
   // groups of up to 8 windows share one pass over the table
   for (int k0 = 0; k0 < n_windows; k0 += 8) {
     const int nk = n_windows - k0 < 8 ? n_windows - k0 : 8;
@@ -345,6 +413,7 @@ int ssb_window_fused(const void* in, int in_dtype, int64_t rows, int64_t cols, i
     return fail(SSB_EINVAL, "missing output buffer");
   if (out_ld < cols - w + 1) return fail(SSB_EINVAL, "out_ld < output cols");
   WinOut o{out_sum, out_mean, out_std, out_ld};
+  SSB_DEVICE_GUARD(stream);
   cudaError_t e = launch_window_fused(in, in_dtype, rows, cols, in_ld, w, stat_mask, o, nonfinite_flag, segments,
                                       as_stream(stream));
   return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_window_fused");
@@ -359,6 +428,7 @@ int ssb_window_sum_at(const void* sat, int is_float_table, int64_t rows, int64_t
   uint64_t c[4];
   const int64_t idx[4] = {(top + w) * sat_ld + left + w, top * sat_ld + left + w, (top + w) * sat_ld + left,
                           top * sat_ld + left};
+  SSB_DEVICE_GUARD(stream);
   cudaStream_t st = as_stream(stream);
   for (int k = 0; k < 4; ++k) {
     cudaError_t e = cudaMemcpyAsync(&c[k], t + idx[k], 8, cudaMemcpyDeviceToHost, st);
@@ -379,7 +449,8 @@ int ssb_window_sum_at(const void* sat, int is_float_table, int64_t rows, int64_t
 }
 
 // ---------------------------------------------------------------------------
-// host-buffer end-to-end path
+// host-buffer end-to-end path (helpers host_sets / host_pool above)
+
 int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
                  int64_t stride, int stat_mask, void* out_sum_host, double* out_mean_host, double* out_std_host,
                  int64_t out_ld, int pipeline, int device, int64_t band_rows) {
@@ -414,7 +485,9 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   }
   if (band_rows > out_r) band_rows = out_r;
   const int64_t n_bands = (out_r + band_rows - 1) / band_rows;
-  const int n_sets = n_bands > 1 ? 2 : 1;
+  // buffer sets in flight (one stream each): the D2H of the results is the
+  // critical path, so a set's H2D + compute overlaps the other sets' D2H
+  const int n_sets = (int)(n_bands < host_sets() ? n_bands : host_sets());
   const int64_t max_in_rows = in_rows_for(band_rows);
 
   const size_t in_bytes = (size_t)max_in_rows * cols * es;
@@ -430,19 +503,17 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   std::vector<Set> sets(n_sets);
   int* d_flag = nullptr;
   int status = SSB_OK;
+  // band buffers come from a library-private stream-ordered pool, trimmed
+  // back to zero before returning: the caller's default pool (and torch's
+  // allocator) never see a changed release threshold or memory kept reserved
+  cudaMemPool_t pool = nullptr;
+  if ((e = host_pool(device, &pool)) != cudaSuccess) return cuda_fail(e, "memory pool");
   auto alloc = [&](void** p, size_t n, cudaStream_t st) -> bool {
     if (n == 0) return true;
-    cudaError_t ae = cudaMallocAsync(p, n, st);
+    cudaError_t ae = cudaMallocFromPoolAsync(p, n, pool, st);
     if (ae != cudaSuccess) { status = cuda_fail(ae, "device allocation"); return false; }
     return true;
   };
-  {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep freed blocks cached across calls
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   for (auto& s : sets) {
     if ((e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking)) != cudaSuccess) { status = cuda_fail(e, "stream"); break; }
     if (!alloc(&s.in, in_bytes, s.st) || !alloc(&s.sat, sat_bytes, s.st) || !alloc(&s.sq, sq ? sat_bytes : 0, s.st) ||
@@ -499,6 +570,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     cudaStreamSynchronize(s.st);
     cudaStreamDestroy(s.st);
   }
+  cudaMemPoolTrimTo(pool, 0);
   if (d_flag) {
     int h = 0;
     if (status == SSB_OK) {

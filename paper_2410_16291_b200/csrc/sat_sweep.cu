@@ -585,27 +585,65 @@ bool sweep_uses_fused(int dtype, int64_t R, int64_t C, int64_t w) {
   return R * C >= ((int64_t)1 << 24) && ((dtype == IN_U8 && w <= 256) || (dtype == IN_U16 && w <= 128));
 }
 
-// Per-thread, per-device side stream and fork/join events (thread-local so
-// concurrent callers never join on each other's fork points).
+// Side streams for the fork/join of ssb_sat_build_swa: a small thread-local
+// pool keyed by the caller's stream (so two caller streams never wait on each
+// other's fork points), each entry on the caller stream's device.  Entries are
+// created whole (stream and both events) before they are published and
+// destroyed with the thread.
 struct SideStream {
+  cudaStream_t caller = nullptr;
+  int dev = -1;
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  unsigned long long last_use = 0;
 };
-static thread_local SideStream t_side[64];
 
-static cudaError_t side_stream(SideStream*& out) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  SideStream& c = t_side[dev];
-  if (!c.s) {
-    if ((e = cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+struct SidePool {
+  static constexpr int kMax = 8;
+  SideStream e[kMax];
+  unsigned long long tick = 0;
+  static void release(SideStream& c) {
+    if (c.fork) cudaEventDestroy(c.fork);
+    if (c.join) cudaEventDestroy(c.join);
+    if (c.s) cudaStreamDestroy(c.s);
+    c = SideStream{};
   }
-  out = &c;
-  return cudaSuccess;
+  ~SidePool() {
+    for (auto& c : e) release(c);
+  }
+};
+static thread_local SidePool t_side;
+
+static cudaError_t side_stream(cudaStream_t caller, SideStream*& out) {
+  int dev = 0;
+  cudaError_t e = cudaStreamGetDevice(caller, &dev);
+  if (e != cudaSuccess) return e;
+  SidePool& pool = t_side;
+  SideStream* victim = &pool.e[0];
+  for (auto& c : pool.e) {
+    if (c.s && c.caller == caller && c.dev == dev) {
+      c.last_use = ++pool.tick;
+      out = &c;
+      return cudaSuccess;
+    }
+    if (!c.s || (victim->s && c.last_use < victim->last_use)) victim = &c;
+  }
+  // the least recently used entry (its pending work keeps running; a reused
+  // stream only orders new work after it)
+  SideStream fresh;
+  fresh.caller = caller;
+  fresh.dev = dev;
+  if ((e = cudaStreamCreateWithFlags(&fresh.s, cudaStreamNonBlocking)) == cudaSuccess &&
+      (e = cudaEventCreateWithFlags(&fresh.fork, cudaEventDisableTiming)) == cudaSuccess &&
+      (e = cudaEventCreateWithFlags(&fresh.join, cudaEventDisableTiming)) == cudaSuccess) {
+    SidePool::release(*victim);
+    *victim = fresh;
+    victim->last_use = ++pool.tick;
+    out = victim;
+    return cudaSuccess;
+  }
+  SidePool::release(fresh);
+  return e;
 }
 
 // table + window statistics: the table build on the caller's stream with the
@@ -620,7 +658,7 @@ cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, in
       return launch_window_eval(sat, nullptr, false, dtype, R, C, sat_ld, w, 1, mask, o, st);
     }
     SideStream* side = nullptr;
-    cudaError_t e = side_stream(side);
+    cudaError_t e = side_stream(st, side);
     if (e != cudaSuccess) return e;
     if ((e = cudaEventRecord(side->fork, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(side->s, side->fork, 0)) != cudaSuccess) return e;

@@ -116,6 +116,7 @@ def allocate_table(elem_kind: ElemKind, rows: int, cols: int, squared: bool, dev
     return _device.empty((rows + 1, _engine.sat_ld_for(cols)), dt, device, what), kind
 
 
+@_engine.device_scoped
 def _build(img: ImageGrid, squared: bool) -> IntegralImage:
     if img.elem_kind is ElemKind.I32 and squared:
         raise TypeError("squared tables are not supported for int32 input")
@@ -156,6 +157,7 @@ def window_sum(sat: IntegralImage, top: int, left: int, w: int):
     return raw[0]
 
 
+@_engine.device_scoped
 def swa_with_table(img: ImageGrid, win: WindowSpec, stat: StatKind) -> tuple[IntegralImage, ResultGrid]:
     """build_sat(img) and swa_integral(img, win, stat) from one pass over the raster.
 
@@ -184,6 +186,7 @@ def _finish(img: ImageGrid, stats, res) -> dict:
     return out
 
 
+@_engine.device_scoped
 def _run_tables(img: ImageGrid, wins, stat: StatKind):
     """Tables once, then the corner sweep(s) (integral.py:166-189, :199-210).
 

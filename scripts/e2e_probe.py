@@ -1,43 +1,63 @@
-"""End-to-end (pinned host in/out) C5 through ssb_swa_host: PCIe ceilings and band sizes (tuning only)."""
+"""e2e probe: pinned PCIe ceilings and ssb_swa_host at C5 (band rows / buffer sets from argv/env).
+
+python scripts/e2e_probe.py [band_rows ...]   (SSB_HOST_SETS selects the buffer-set count)"""
+import json
+import os
 import sys
 import time
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 
-from paper_2410_16291_b200 import _lib, synthetic
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2410_16291_b200 as sb  # noqa: E402
+from paper_2410_16291_b200 import _engine, synthetic  # noqa: E402
+from paper_2410_16291_b200.grid import ImageGrid, StatKind  # noqa: E402
 
-rows, cols, w = 70000, 85000, 256
-lib = _lib.load()
-dev = torch.device("cuda", 0)
-oc, orr = cols - w + 1, rows - w + 1
-hin = torch.empty((rows, cols), dtype=torch.uint8, pin_memory=True)
-hin.numpy()[:] = synthetic.c5()
-hout = torch.empty((orr, oc), dtype=torch.int64, pin_memory=True)
 
-g = torch.empty(4 << 30, dtype=torch.uint8, device=dev)
-hb = torch.empty(4 << 30, dtype=torch.uint8, pin_memory=True)
-for name, fn in (("D2H", lambda: hb.copy_(g, non_blocking=True)), ("H2D", lambda: g.copy_(hb, non_blocking=True))):
-    fn()
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    for _ in range(3):
-        fn()
-    torch.cuda.synchronize()
-    print(f"{name} pinned 4 GiB: {3 * (4 << 30) / (time.perf_counter() - t) / 1e9:.1f} GB/s", flush=True)
-del g, hb
-torch.cuda.empty_cache()
+def pcie(nbytes=4 << 30, streams=1, reps=3):
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    ss = [torch.cuda.Stream() for _ in range(streams)]
+    chunk = nbytes // streams
+    res = {}
+    for name, fn in (("d2h", lambda s, a, b: h[a:b].copy_(d[a:b], non_blocking=True)),
+                     ("h2d", lambda s, a, b: d[a:b].copy_(h[a:b], non_blocking=True))):
+        best = 0
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for k, s in enumerate(ss):
+                with torch.cuda.stream(s):
+                    fn(s, k * chunk, (k + 1) * chunk)
+            torch.cuda.synchronize()
+            best = max(best, nbytes / (time.perf_counter() - t0) / 1e9)
+        res[name] = best
+    del d, h
+    return res
 
-for band in (0, 1024, 2048, 8192):
-    def call():
-        _lib.check(lib.ssb_swa_host(hin.data_ptr(), 0, rows, cols, cols, w, 1, 1, hout.data_ptr(), None, None, oc,
-                                    0, 0, band))
-    call()
-    t = time.perf_counter()
-    for _ in range(2):
-        call()
-    dt = (time.perf_counter() - t) / 2
-    print(f"ssb_swa_host band_rows={band}: {dt:.3f} s  {rows * cols / dt / 1e9:.2f} Gpx/s  "
-          f"(D2H-equivalent {orr * oc * 8 / dt / 1e9:.1f} GB/s)", flush=True)
+
+def main():
+    bands = [int(a) for a in sys.argv[1:]] or [0]
+    print(json.dumps({"pcie_1stream": pcie(streams=1), "pcie_2streams": pcie(streams=2),
+                      "sets": os.environ.get("SSB_HOST_SETS", "default")}), flush=True)
+    img = synthetic.c5(threads=os.cpu_count())
+    hin = torch.empty(img.shape, dtype=torch.uint8, pin_memory=True)
+    hin.numpy()[...] = img
+    del img
+    out_r, out_c = 70000 - 255, 85000 - 255
+    hout = torch.empty((out_r, out_c), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+    grid = ImageGrid(hin.numpy(), _check_finite=False)
+    for br in bands:
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            _engine.run_host(grid, 256, 1, [StatKind.SUM], "table", outs={StatKind.SUM: hout}, band_rows=br)
+            ts.append(time.perf_counter() - t0)
+        print(json.dumps({"band_rows": br, "s": ts, "gpx_s": 5.95 / min(ts), "d2h_gbs": out_r * out_c * 8 / min(ts) / 1e9}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -338,6 +338,51 @@ def test_capi_rejects_unaligned_raster(sb):
     assert rc == _lib.EINVAL and b"aligned" in lib.ssb_last_error()
 
 
+def test_capi_table_writers_reject_pitch_2_mod_4(sb):
+    """Table rows are written with 256-bit stores: a pitch of 2 mod 4 elements
+    (cols + 1 rounded up to even, e.g. C5's 85,002) or a table that is not
+    32-byte aligned is refused with SSB_EINVAL before any launch, and the
+    context stays usable (no misaligned-address fault)."""
+    import torch
+
+    from paper_2410_16291_b200 import _device, _engine, _lib
+
+    lib = _lib.load()
+    R, C = 37, 85  # cols + 1 = 86 = 2 mod 4
+    v = np.random.default_rng(11).integers(0, 256, (R, C), dtype=np.uint8)
+    x = to_dev(v)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream().cuda_stream
+    bad_ld = C + 1
+    assert bad_ld % 4 == 2
+    sat = _device.empty((R + 1, 90), np.uint64, dev, "t")
+    wsb = max(int(lib.ssb_sat_workspace_bytes(_lib.U8, R, C, 0)), int(lib.ssb_sat_swa_workspace_bytes(_lib.U8, R, C)),
+              int(lib.ssb_sat_lookback_workspace_bytes(_lib.U8, R, C, 0)))
+    ws = _device.empty((wsb,), np.uint8, dev, "ws")
+    out = _device.empty((R - 4, C - 4), np.uint64, dev, "o")
+    calls = {
+        "build": lambda ld, p: lib.ssb_sat_build(x.data_ptr(), _lib.U8, R, C, C, p, None, ld, None, None,
+                                                 ws.data_ptr(), wsb, None, st),
+        "finish": lambda ld, p: lib.ssb_sat_finish(x.data_ptr(), _lib.U8, R, C, C, p, None, ld, None, None,
+                                                   ws.data_ptr(), wsb, st),
+        "lookback": lambda ld, p: lib.ssb_sat_build_lookback(x.data_ptr(), _lib.U8, R, C, C, p, None, ld, None, None,
+                                                             ws.data_ptr(), wsb, st),
+        "swa": lambda ld, p: lib.ssb_sat_build_swa(x.data_ptr(), _lib.U8, R, C, C, p, ld, 5, _lib.SUM, out.data_ptr(),
+                                                   None, C - 4, ws.data_ptr(), wsb, st),
+    }
+    for name, fn in calls.items():
+        assert fn(bad_ld, sat.data_ptr()) == _lib.EINVAL, name
+        assert b"multiple of 4" in lib.ssb_last_error(), name
+        assert fn(88, sat.data_ptr() + 16) == _lib.EINVAL, name  # 16- but not 32-byte aligned
+        assert b"32-byte" in lib.ssb_last_error(), name
+    # the rounded pitch works and the context is healthy
+    ld = _engine.sat_ld_for(C)
+    assert ld % 4 == 0
+    assert calls["build"](ld, sat.data_ptr()) == _lib.OK
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(host(sat, np.uint64)[:, : C + 1], O.build_table(v))
+
+
 def test_concurrent_threads(sb):
     """The facade is reentrant: concurrent callers get correct, independent results."""
     import threading

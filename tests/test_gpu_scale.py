@@ -1,0 +1,291 @@
+"""Whole-output and whole-table parity at BASELINE.json sizes (C2-C5).
+
+The reference cannot hold C5 whole (about 148 GB with its sweep temporaries,
+SURVEY.md 8c), so every comparison here is banded on the host:
+
+* window outputs: output rows [lo, hi) against the oracle's ``swa_threaded``
+  (the reference's ``swa_parallel``, parallel.py:137-149) on input rows
+  [lo, hi + w - 1) -- bit-identical to the whole-image result because table
+  offsets cancel in the four-corner difference;
+* integral images: table rows (a, b] against the oracle's ``build_table``
+  (integral.py:109-116) of image rows [a, b) plus the carry row a (the table
+  row above the band, itself checked by the previous band, starting from the
+  zero border).  Integer tables are uint64 modulo 2^64 on both sides, so the
+  banded oracle equals the reference's whole table bit for bit; float64 tables
+  differ only in summation order and are held to a relative tolerance.
+
+The window sums alone cannot see per-row or per-column table offsets (they
+cancel), so the table checks are what pins the integral image that the
+headline step writes.  At C5 the corner-sweep pipeline (ssb_window_eval) then
+reads the verified table back and must reproduce the verified window sums.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from oracle import satsweep_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = os.cpu_count() or 1
+# F64 tables: summation order differs from the reference's cumsum order; the
+# values are sums of positive pixels, so the relative error stays ~1e-12.
+TABLE_RTOL_F64 = 1e-9
+# F32 mean/std: north_star tolerance for fp64 accumulation
+STAT_RTOL_F32 = 1e-6
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2410_16291_b200 import _lib, build_ext
+
+    build_ext.build()
+    _lib.load()
+    import paper_2410_16291_b200 as mod
+
+    return mod
+
+
+@pytest.fixture(scope="module")
+def pool():
+    with ThreadPoolExecutor(P) as p:
+        yield p
+
+
+@pytest.fixture(autouse=True)
+def _free_device():
+    import torch
+
+    from paper_2410_16291_b200 import _engine
+
+    _engine.release_scratch()
+    yield
+    _engine.release_scratch()
+    torch.cuda.empty_cache()
+
+
+def _chunks(n: int, p: int = P):
+    step = max(1, -(-n // p))
+    return [(a, min(n, a + step)) for a in range(0, n, step)]
+
+
+def par_equal(a: np.ndarray, b: np.ndarray, pool) -> bool:
+    assert a.shape == b.shape, (a.shape, b.shape)
+    return all(pool.map(lambda ab: bool(np.array_equal(a[ab[0]:ab[1]], b[ab[0]:ab[1]])), _chunks(a.shape[0])))
+
+
+def par_max_rel(a: np.ndarray, b: np.ndarray, pool) -> float:
+    """max |a - b| / |b| over the grid; a difference where b == 0 counts as inf."""
+    assert a.shape == b.shape, (a.shape, b.shape)
+
+    def f(ab):
+        x, y = a[ab[0]:ab[1]], b[ab[0]:ab[1]]
+        d = np.abs(x - y)
+        nz = d > 0
+        if not nz.any():
+            return 0.0
+        den = np.abs(y[nz])
+        if not (den > 0).all():
+            return float("inf")
+        return float((d[nz] / den).max())
+
+    return max(pool.map(f, _chunks(a.shape[0])))
+
+
+class Pinned:
+    """One reusable pinned host buffer for band read-backs."""
+
+    def __init__(self):
+        self.buf = None
+
+    def rows(self, t, a: int, b: int, np_dtype):
+        import torch
+
+        src = t[a:b]
+        nbytes = src.numel() * src.element_size()
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = None
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        dst = self.buf[:nbytes].view(src.dtype).view(src.shape)
+        dst.copy_(src)
+        return dst.numpy().view(np.dtype(np_dtype))
+
+
+def check_table(dev_table, img: np.ndarray, squared: bool, pool, band: int, pinned: Pinned,
+                rtol: float | None = None) -> dict:
+    """Whole (rows+1) x (cols+1) device table against the banded oracle; returns stats."""
+    rows, cols = img.shape
+    acc = np.float64 if img.dtype == np.float32 else (np.int64 if img.dtype == np.int32 else np.uint64)
+    top = pinned.rows(dev_table, 0, 1, acc)[0, : cols + 1].copy()
+    assert not top.any(), "table row 0 must be the zero border"
+    carry = top
+    worst = 0.0
+    for a in range(0, rows, band):
+        b = min(rows, a + band)
+        ref = O.build_table(img[a:b], squared, P, P, pool)[1:]  # local table rows 1..b-a of the band
+        ref_c = ref  # add the carry row (the global table row a) in place, row blocks in parallel
+        list(pool.map(lambda rr: np.add(ref_c[rr[0]:rr[1]], carry, out=ref_c[rr[0]:rr[1]]), _chunks(b - a)))
+        got = pinned.rows(dev_table, a + 1, b + 1, acc)[:, : cols + 1]
+        assert not got[:, 0].any(), f"zero border column broken in rows {a + 1}..{b}"
+        if rtol is None:
+            assert par_equal(got, ref, pool), f"table rows {a + 1}..{b} differ from the oracle"
+        else:
+            e = par_max_rel(got, ref, pool)
+            worst = max(worst, e)
+            assert e <= rtol, f"table rows {a + 1}..{b}: max rel err {e:.3g} > {rtol}"
+        carry = got[-1].copy()  # verified row b is the next band's carry
+        del ref, got
+    # the last row's increments are the image's column totals (an independent
+    # host reduction; exact for integers)
+    if rtol is None and not squared:
+        col_tot = np.zeros(cols, dtype=acc)
+        for a, b in _chunks(rows, 8):
+            col_tot += np.sum(img[a:b], axis=0, dtype=acc)
+        assert np.array_equal(np.diff(carry), col_tot), "last table row != column totals of the image"
+    return {"max_rel": worst}
+
+
+def check_outputs(dev_out, img: np.ndarray, w: int, stat: str, pool, band: int, pinned: Pinned,
+                  rtol: float | None = None) -> float:
+    """Whole device output grid against the oracle's swa_threaded, band by band."""
+    out_r = img.shape[0] - w + 1
+    dt = {"sum": (np.float64 if img.dtype == np.float32 else (np.int64 if img.dtype == np.int32 else np.uint64))}.get(
+        stat, np.float64)
+    assert tuple(dev_out.shape) == (out_r, img.shape[1] - w + 1)
+    worst = 0.0
+    for lo in range(0, out_r, band):
+        hi = min(out_r, lo + band)
+        ref = O.swa_threaded(img[lo:hi + w - 1], w, stat, 1, P)
+        got = pinned.rows(dev_out, lo, hi, dt)
+        if rtol is None:
+            assert par_equal(got, ref.astype(dt, copy=False), pool), f"{stat} rows {lo}..{hi} differ"
+        else:
+            e = par_max_rel(got, ref, pool)
+            worst = max(worst, e)
+            assert e <= rtol, f"{stat} rows {lo}..{hi}: max rel err {e:.3g} > {rtol}"
+        del ref, got
+    return worst
+
+
+def _dev_equal_rows(a, b, band: int = 2048) -> bool:
+    import torch
+
+    return all(bool(torch.equal(a[r:r + band], b[r:r + band])) for r in range(0, a.shape[0], band))
+
+
+# ----------------------------------------------------------------------------- C5 (headline)
+def test_c5_whole_table_and_windows(sb, pool):
+    """The headline step's two products at full C5 size: the whole 70,001 x 85,001
+    integral image and the whole 69,745 x 84,745 window-sum grid, each bit-exact
+    against the banded oracle; then the corner sweep reads the table back."""
+    import torch
+
+    from paper_2410_16291_b200 import _engine, synthetic
+    from paper_2410_16291_b200.grid import ElemKind, ImageGrid, StatKind, WindowSpec
+    from paper_2410_16291_b200.integral import swa_with_table
+
+    t0 = time.perf_counter()
+    img = synthetic.c5(threads=P)
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(img).to(dev)
+    table, res = swa_with_table(ImageGrid(x), WindowSpec(256), StatKind.SUM)  # ssb_sat_build_swa
+    out = res.values
+    torch.cuda.synchronize()
+    pinned = Pinned()
+    check_table(table.device_table, img, False, pool, 4096, pinned)
+    t_tab = time.perf_counter()
+    check_outputs(out, img, 256, "sum", pool, 4096, pinned)
+    t_out = time.perf_counter()
+    # corner sweep (the reference's structure): the verified table read back
+    out2 = _engine.eval_tables(table.device_table, None, table.pitch, ElemKind.U8, 70000, 85000, 256, 1,
+                               [StatKind.SUM], dev)[StatKind.SUM]
+    assert _dev_equal_rows(out2, out)
+    print(f"C5 whole: table {t_tab - t0:.1f} s, outputs {t_out - t_tab:.1f} s, sweep {time.perf_counter() - t_out:.1f} s")
+    del out2, out, table, res, x
+
+
+def test_c5_onepass_kernel_whole(sb, pool):
+    """The one-pass table+windows kernel (ssb_sat_build_swa_onepass) at full C5:
+    whole table and whole window grid bit-exact against the banded oracle."""
+    import torch
+
+    from paper_2410_16291_b200 import _engine, synthetic
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    img = synthetic.c5(threads=P)
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(img).to(dev)
+    sat, ld, outs = _engine.table_and_sweep(x, ElemKind.U8, 70000, 85000, 256, (StatKind.SUM,), dev, onepass=True)
+    torch.cuda.synchronize()
+    pinned = Pinned()
+    check_table(sat, img, False, pool, 4096, pinned)
+    check_outputs(outs[StatKind.SUM], img, 256, "sum", pool, 4096, pinned)
+    del sat, outs, x
+
+
+# ----------------------------------------------------------------------------- C4 (float)
+@pytest.mark.parametrize("pipe", ["table", "fused"])
+def test_c4_whole_mean_std(sb, pool, pipe):
+    """All 19,937 x 23,937 means and stds of C4, both pipelines, within rtol 1e-6."""
+    import torch
+
+    from paper_2410_16291_b200 import synthetic
+
+    img = synthetic.c4()
+    x = torch.from_numpy(img).to("cuda:0")
+    res = sb.swa_stats(x, 64, ("mean", "std"), pipeline=pipe)
+    pinned = Pinned()
+    e_mean = check_outputs(res["mean"], img, 64, "mean", pool, 4096, pinned, rtol=STAT_RTOL_F32)
+    e_std = check_outputs(res["std"], img, 64, "std", pool, 4096, pinned, rtol=STAT_RTOL_F32)
+    print(f"C4 {pipe}: max rel err mean {e_mean:.3g}, std {e_std:.3g}")
+    del res, x
+
+
+def test_c4_whole_tables(sb, pool):
+    """C4's two float64 tables (plain and squared), whole, within rtol 1e-9."""
+    import torch
+
+    from paper_2410_16291_b200 import synthetic
+
+    img = synthetic.c4()
+    x = torch.from_numpy(img).to("cuda:0")
+    pinned = Pinned()
+    for squared in (False, True):
+        t = sb.build_sat(sb.ImageGrid(x), squared)
+        st = check_table(t.device_table, img, squared, pool, 4096, pinned, rtol=TABLE_RTOL_F64)
+        print(f"C4 table squared={squared}: max rel err {st['max_rel']:.3g}")
+        del t
+
+
+# ----------------------------------------------------------------------------- C3 / C2 (integer)
+def test_c3_whole_table(sb, pool):
+    """C3's shared 30,001 x 30,001 table (the one multi_window sweeps), whole, bit-exact."""
+    import torch
+
+    from paper_2410_16291_b200 import synthetic
+
+    img = synthetic.c3()
+    x = torch.from_numpy(img).to("cuda:0")
+    t = sb.build_sat(sb.ImageGrid(x))
+    check_table(t.device_table, img, False, pool, 8192, Pinned())
+
+
+def test_c2_whole_table_int32(sb, pool):
+    """C2's int32 raster: the int64 table, whole, bit-exact."""
+    import torch
+
+    from paper_2410_16291_b200 import synthetic
+
+    img = synthetic.c2()
+    x = torch.from_numpy(img).to("cuda:0")
+    t = sb.build_sat(sb.ImageGrid(x))
+    check_table(t.device_table, img, False, pool, 10000, Pinned())
