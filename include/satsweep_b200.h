@@ -187,6 +187,58 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
                  int64_t stride, int stat_mask, void* out_sum_host, double* out_mean_host, double* out_std_host,
                  int64_t out_ld, int pipeline, int device, int64_t band_rows);
 
+/* ---- row-band sharding over several GPUs ----------
+ * Replaces the reference's worker fan-out of one process
+ * (swa(method="parallel"), api.py:51-52 -> swa_parallel / build_sat_parallel /
+ * parallel_sweep, parallel.py:80-149): device g owns a contiguous band of
+ * image rows by the reference's partition rule over OUTPUT rows
+ * (parallel.py:80-90).
+ *
+ * ssb_sharded_plan: plan7[7*g .. 7*g+6] = {own_lo, own_hi, need_lo, need_hi,
+ * out_lo, out_hi, cap_rows}: image rows [own_lo, own_hi) are OWNED by device g
+ * (a partition of [0, rows)); its output rows [out_lo, out_hi) need image rows
+ * [need_lo, need_hi) (own rows + the (w-1)-row halo below); its band buffer
+ * holds cap_rows rows starting at global row own_lo.  Pure host function. */
+int ssb_sharded_plan(int64_t rows, int64_t cols, int64_t w, int ndev, int64_t* plan7);
+
+/* Scratch for band `band` of ssb_sharded_swa (with_table: the global-table
+ * workspace + the gathered column totals; 8 bytes when no table is built). */
+int64_t ssb_sharded_workspace_bytes(int in_dtype, int64_t rows, int64_t cols, int64_t w, int ndev, int band,
+                                    int with_table);
+
+/* Window statistics (stride 1) and, with `sats`, the GLOBAL integral image
+ * of a rows x cols image sharded over ndev devices of this process.  Per
+ * device g (every array indexed by g; devs[g] may repeat a device):
+ *   bands[g]   device buffer of cap_rows x cols on devs[g]; the caller fills the
+ *              own rows (row 0 = global row own_lo) and the library writes the
+ *              halo rows after them, copied from the following devices' own
+ *              rows by peer copies (NVLink P2P) -- the halo exchange;
+ *   sats[g]    (nullable array) (own_hi - own_lo + 1) x sat_ld table, 32-byte
+ *              aligned, sat_ld a multiple of 4: global table rows
+ *              [own_lo, own_hi] (row 0 is the carry row = the table row above
+ *              the band).  Built from the band's column totals, gathered from
+ *              the devices above by peer copies and summed in band order
+ *              (the exclusive scan of per-band column-total vectors);
+ *   out_*[g]   the band's output rows [out_lo, out_hi) at pitch out_ld;
+ *   ws[g]      ssb_sharded_workspace_bytes(..., g, sats != NULL) bytes;
+ *   streams[g] a stream on devs[g]; all work is asynchronous on it, and every
+ *              stream is joined with every other before the call returns, so
+ *              the caller may reuse any buffer in stream order.
+ * stat_mask may be 0 (table only).  F32 finiteness is not checked here (use
+ * ssb_f32_nonfinite on each band).  w <= ssb_window_fused_max_w(). */
+int ssb_sharded_swa(int ndev, const int* devs, int in_dtype, int64_t rows, int64_t cols, int64_t w, int stat_mask,
+                    void* const* bands, void* const* sats, int64_t sat_ld, void* const* out_sum,
+                    double* const* out_mean, double* const* out_std, int64_t out_ld, void* const* ws,
+                    const int64_t* ws_bytes, void* const* streams);
+
+/* carry[c] = sum_{g < band} parts[g * parts_ld + c] for c < len (uint64
+ * modulo 2^64, or double when is_float), summed in g order: the exclusive
+ * scan over row bands of their column-total vectors, for multi-process
+ * callers that gathered the totals themselves (e.g. an NCCL all-gather of
+ * ssb_sat_prepare's band_totals); the result is ssb_sat_finish's carry. */
+int ssb_band_carry(const void* parts, int band, int64_t len, int64_t parts_ld, int is_float, void* carry,
+                   void* stream);
+
 /* Count of kernel launches the library issued since load (diagnostics). */
 int64_t ssb_launch_count(void);
 

@@ -58,6 +58,15 @@ _SIGS = {
     "ssb_window_fused": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _i64, _vp, _int, _vp]),
     "ssb_window_sum_at": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "ssb_swa_host": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _i64, _int, _int, _i64]),
+    "ssb_sharded_plan": (_int, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64)]),
+    "ssb_sharded_workspace_bytes": (_i64, [_int, _i64, _i64, _i64, _int, _int, _int]),
+    "ssb_sharded_swa": (
+        _int,
+        [_int, ctypes.POINTER(_int), _int, _i64, _i64, _i64, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
+         ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(_vp),
+         ctypes.POINTER(_i64), ctypes.POINTER(_vp)],
+    ),
+    "ssb_band_carry": (_int, [_vp, _int, _i64, _i64, _int, _vp, _vp]),
     "ssb_file_to_device": (_int, [ctypes.c_char_p, _i64, _i64, _vp, _int, _vp]),
     "ssb_device_to_file": (_int, [ctypes.c_char_p, _i64, _vp, _i64, _int, _vp]),
     "ssb_f32_nonfinite": (_int, [_vp, _i64, _vp, _vp]),

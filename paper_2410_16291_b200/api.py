@@ -42,10 +42,27 @@ def _check_method(method: str, threads: int) -> None:
         raise ValueError(f"workers must be >= 0 (0 = auto), got {threads}")
 
 
-def swa_stats(array, window: int, stats=("sum",), stride: int = 1, *, pipeline: str = "auto", out=None) -> dict:
+def _run(img: ImageGrid, win: WindowSpec, kinds, pipeline, outs, devices):
+    if devices is not None:
+        from . import multidev
+
+        if img.on_device:
+            if win.stride != 1:
+                raise ValueError("the multi-device path for CUDA rasters needs stride 1")
+            if outs is not None:
+                raise ValueError("out= is not supported with devices= for CUDA rasters")
+            return multidev.swa_device(img, win.w, kinds, devices)[0]
+        return multidev.swa_host(img, win.w, win.stride, kinds, devices, pipeline, outs=outs)
+    if img.on_device:
+        return _engine.run_device(img, win.w, win.stride, kinds, pipeline, outs=outs)
+    return _engine.run_host(img, win.w, win.stride, kinds, pipeline, outs=outs)
+
+
+def swa_stats(array, window: int, stats=("sum",), stride: int = 1, *, pipeline: str = "auto", out=None,
+              devices=None) -> dict:
     """Several statistics of one window from one pass (e.g. BASELINE C2's sum + mean).
 
-    Returns {stat name: array}."""
+    Returns {stat name: array}.  ``devices``: see ``swa``."""
     img = _as_grid(array)
     win = WindowSpec(window, stride)
     kinds = []
@@ -55,28 +72,27 @@ def swa_stats(array, window: int, stats=("sum",), stride: int = 1, *, pipeline: 
             kinds.append(k)
     win.validate_for(img.rows, img.cols)
     outs = None if out is None else {StatKind.parse(k): v for k, v in out.items()}
-    if img.on_device:
-        res = _engine.run_device(img, win.w, win.stride, kinds, pipeline, outs=outs)
-    else:
-        res = _engine.run_host(img, win.w, win.stride, kinds, pipeline, outs=outs)
+    res = _run(img, win, kinds, pipeline, outs, devices)
     return {k.value: res[k] for k in kinds}
 
 
 def swa(array, window: int, stat: str = "sum", method: str = "parallel", stride: int = 1, threads: int = 0, *,
-        pipeline: str = "auto", out=None):
+        pipeline: str = "auto", out=None, devices=None):
     """Sliding-window statistic over a 2-D array (api.py:28-55).
 
     ``method`` is accepted for compatibility; every method runs the GPU path
-    (the reference guarantees all methods agree).  ``threads`` is ignored."""
+    (the reference guarantees all methods agree).  ``threads`` is ignored.
+    ``devices`` (extension): ``None`` runs on the current GPU (a CUDA raster's
+    own); ``"all"`` or a list of GPUs fans contiguous output-row bands over
+    them from this process, the reference's worker partition
+    (parallel.py:80-90) with GPUs as workers (multidev.py)."""
     img = _as_grid(array)
     win = WindowSpec(window, stride)
     kind = StatKind.parse(stat)
     _check_method(method, threads)
     win.validate_for(img.rows, img.cols)
     outs = None if out is None else {kind: out}
-    if img.on_device:
-        return _engine.run_device(img, win.w, win.stride, [kind], pipeline, outs=outs)[kind]
-    return _engine.run_host(img, win.w, win.stride, [kind], pipeline, outs=outs)[kind]
+    return _run(img, win, [kind], pipeline, outs, devices)[kind]
 
 
 def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str = "table") -> list:

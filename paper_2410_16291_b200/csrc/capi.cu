@@ -52,6 +52,8 @@ constexpr int64_t kFusedMaxWindow = 3072;
 static std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int io_fail(int code, const char* fmt, ...);
+int shard_fail(int code, const char* fmt, ...);
+int shard_cuda_fail(cudaError_t e, const char* where);
 }  // namespace ssb
 
 using namespace ssb;
@@ -141,7 +143,19 @@ struct DeviceGuard {
   if (device_guard_.err != cudaSuccess) return cuda_fail(device_guard_.err, "stream device")
 }  // namespace
 
-// io.cu reports through the same thread-local message
+// shard.cu and io.cu report through the same thread-local message
+int ssb::shard_fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+int ssb::shard_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+
 int ssb::io_fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -496,11 +510,17 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   const size_t out_bytes = (size_t)band_rows * out_c * 8;
 
   struct Set {
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr;         // H2D + compute of this set's bands
+    cudaEvent_t ready = nullptr;       // band results complete (recorded on st)
+    cudaEvent_t drained = nullptr;     // band results copied out (recorded on the D2H stream)
     void *in = nullptr, *sat = nullptr, *sq = nullptr, *ws = nullptr, *o_sum = nullptr, *o_mean = nullptr,
          *o_std = nullptr;
   };
   std::vector<Set> sets(n_sets);
+  // every D2H goes through ONE stream in band order: the result copy is the
+  // critical path, and a single in-order copy stream keeps one copy engine
+  // streaming at the PCIe ceiling while the sets' H2D + compute run beside it
+  cudaStream_t d2h_st = nullptr;
   int* d_flag = nullptr;
   int status = SSB_OK;
   // band buffers come from a library-private stream-ordered pool, trimmed
@@ -514,8 +534,15 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (ae != cudaSuccess) { status = cuda_fail(ae, "device allocation"); return false; }
     return true;
   };
+  if ((e = cudaStreamCreateWithFlags(&d2h_st, cudaStreamNonBlocking)) != cudaSuccess) status = cuda_fail(e, "stream");
   for (auto& s : sets) {
-    if ((e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking)) != cudaSuccess) { status = cuda_fail(e, "stream"); break; }
+    if (status != SSB_OK) break;
+    if ((e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&s.drained, cudaEventDisableTiming)) != cudaSuccess) {
+      status = cuda_fail(e, "stream");
+      break;
+    }
     if (!alloc(&s.in, in_bytes, s.st) || !alloc(&s.sat, sat_bytes, s.st) || !alloc(&s.sq, sq ? sat_bytes : 0, s.st) ||
         !alloc(&s.ws, ws_bytes, s.st) || !alloc(&s.o_sum, (stat_mask & SSB_SUM) ? out_bytes : 0, s.st) ||
         !alloc(&s.o_mean, (stat_mask & SSB_MEAN) ? out_bytes : 0, s.st) ||
@@ -530,6 +557,8 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     const int64_t o0 = b * band_rows, o1 = (o0 + band_rows < out_r) ? o0 + band_rows : out_r;
     const int64_t nb = o1 - o0, r0 = o0 * stride, nr = in_rows_for(nb);
     const char* src = reinterpret_cast<const char*>(in_host) + (size_t)r0 * in_ld * es;
+    // the set's outputs may be overwritten once its previous band is copied out
+    if (b >= n_sets && (e = cudaStreamWaitEvent(s.st, s.drained, 0)) != cudaSuccess) { status = cuda_fail(e, "wait"); break; }
     // contiguous rows: one linear copy (no per-row DMA descriptors)
     e = in_ld == cols ? cudaMemcpyAsync(s.in, src, (size_t)nr * cols * es, cudaMemcpyHostToDevice, s.st)
                       : cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es,
@@ -546,13 +575,17 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       e = launch_window_fused(s.in, in_dtype, nr, cols, cols, w, stat_mask, o, d_flag, 0, s.st);
     }
     if (e != cudaSuccess) { status = cuda_fail(e, "band compute"); break; }
+    if ((e = cudaEventRecord(s.ready, s.st)) != cudaSuccess || (e = cudaStreamWaitEvent(d2h_st, s.ready, 0)) != cudaSuccess) {
+      status = cuda_fail(e, "event");
+      break;
+    }
     auto d2h = [&](void* host, void* dev) -> bool {
       if (!host) return true;
       char* dst = reinterpret_cast<char*>(host) + (size_t)o0 * out_ld * 8;
       cudaError_t ce = out_ld == out_c
-                           ? cudaMemcpyAsync(dst, dev, (size_t)nb * out_c * 8, cudaMemcpyDeviceToHost, s.st)
+                           ? cudaMemcpyAsync(dst, dev, (size_t)nb * out_c * 8, cudaMemcpyDeviceToHost, d2h_st)
                            : cudaMemcpy2DAsync(dst, (size_t)out_ld * 8, dev, (size_t)out_c * 8, (size_t)out_c * 8,
-                                               (size_t)nb, cudaMemcpyDeviceToHost, s.st);
+                                               (size_t)nb, cudaMemcpyDeviceToHost, d2h_st);
       if (ce != cudaSuccess) { status = cuda_fail(ce, "D2H"); return false; }
       return true;
     };
@@ -560,6 +593,11 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
         !d2h((stat_mask & SSB_MEAN) ? out_mean_host : nullptr, s.o_mean) ||
         !d2h((stat_mask & SSB_STD) ? out_std_host : nullptr, s.o_std))
       break;
+    if ((e = cudaEventRecord(s.drained, d2h_st)) != cudaSuccess) { status = cuda_fail(e, "event"); break; }
+  }
+  if (d2h_st) {
+    cudaError_t se = cudaStreamSynchronize(d2h_st);
+    if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");
   }
   for (auto& s : sets) {
     if (!s.st) continue;
@@ -568,8 +606,11 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     void* ptrs[] = {s.in, s.sat, s.sq, s.ws, s.o_sum, s.o_mean, s.o_std};
     for (void* p : ptrs) if (p) cudaFreeAsync(p, s.st);
     cudaStreamSynchronize(s.st);
+    if (s.ready) cudaEventDestroy(s.ready);
+    if (s.drained) cudaEventDestroy(s.drained);
     cudaStreamDestroy(s.st);
   }
+  if (d2h_st) cudaStreamDestroy(d2h_st);
   cudaMemPoolTrimTo(pool, 0);
   if (d_flag) {
     int h = 0;

@@ -599,7 +599,7 @@ struct SideStream {
 };
 
 struct SidePool {
-  static constexpr int kMax = 8;
+  static constexpr int kMax = 16;
   SideStream e[kMax];
   unsigned long long tick = 0;
   static void release(SideStream& c) {
@@ -646,6 +646,24 @@ static cudaError_t side_stream(cudaStream_t caller, SideStream*& out) {
   return e;
 }
 
+// Fork a side stream off `st` (it waits for st's work so far) / join it back
+// (st waits for the side stream's work so far).
+cudaError_t side_fork(cudaStream_t st, SideHandle* h) {
+  SideStream* side = nullptr;
+  cudaError_t e = side_stream(st, side);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaEventRecord(side->fork, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(side->s, side->fork, 0)) != cudaSuccess) return e;
+  h->s = side->s;
+  h->join = side->join;
+  return cudaSuccess;
+}
+
+cudaError_t side_join(cudaStream_t st, const SideHandle& h) {
+  cudaError_t e = cudaEventRecord(h.join, h.s);
+  return e == cudaSuccess ? cudaStreamWaitEvent(st, h.join, 0) : e;
+}
+
 // table + window statistics: the table build on the caller's stream with the
 // fused window kernel on a forked side stream, or reduce + carries then the
 // one-pass table+sweep kernel
@@ -657,16 +675,13 @@ cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, in
       if (e != cudaSuccess) return e;
       return launch_window_eval(sat, nullptr, false, dtype, R, C, sat_ld, w, 1, mask, o, st);
     }
-    SideStream* side = nullptr;
-    cudaError_t e = side_stream(st, side);
+    SideHandle side;
+    cudaError_t e = side_fork(st, &side);
     if (e != cudaSuccess) return e;
-    if ((e = cudaEventRecord(side->fork, st)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(side->s, side->fork, 0)) != cudaSuccess) return e;
     e = launch_sat_build(dtype, in, R, C, in_ld, sat, nullptr, sat_ld, nullptr, nullptr, ws, nullptr, st);
-    const cudaError_t ef = launch_window_fused(in, dtype, R, C, in_ld, w, mask, o, nullptr, 0, side->s);
+    const cudaError_t ef = launch_window_fused(in, dtype, R, C, in_ld, w, mask, o, nullptr, 0, side.s);
     // always join, so the caller's stream never runs ahead of the side stream
-    const cudaError_t er = cudaEventRecord(side->join, side->s);
-    const cudaError_t ew = er == cudaSuccess ? cudaStreamWaitEvent(st, side->join, 0) : er;
+    const cudaError_t ew = side_join(st, side);
     return e != cudaSuccess ? e : ef != cudaSuccess ? ef : ew;
   }
   const SweepPlan sp = make_sweep_plan(dtype, R, C, w);

@@ -126,17 +126,20 @@ def halo_exchange(band, rows: int, w: int, stride: int, group=None, storage=None
     a_own, b_own = owned[rank]
     assert band.shape[0] == b_own - a_own, (band.shape, owned[rank])
     a_need, b_need = need[rank]
-    if n == 1 or b_need <= a_need:
+    if n == 1:
         return band[max(0, a_need - a_own):max(0, b_need - a_own)]
+    # a rank with no output rows receives nothing but still sends its rows to
+    # the ranks whose windows reach into them
+    empty = b_need <= a_need
     base = None  # global row held by storage[0]
-    if storage is not None:
+    if storage is not None and not empty:
         base = min(a_own, a_need)
         assert storage.shape[0] >= max(b_own, b_need) - base
         assert band.data_ptr() == storage[a_own - base:].data_ptr(), "band must be the owned-rows view of storage"
     ops, recv = [], []
     # what I receive: rows of [a_need, b_need) owned by other ranks
     for src in range(n):
-        if src == rank:
+        if src == rank or empty:
             continue
         a, b = owned[src]
         lo, hi = max(a, a_need), min(b, b_need)
@@ -158,6 +161,8 @@ def halo_exchange(band, rows: int, w: int, stride: int, group=None, storage=None
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    if empty:
+        return band[:0]
     if base is not None:
         return storage[a_need - base:b_need - base]
     pieces = []
@@ -169,62 +174,121 @@ def halo_exchange(band, rows: int, w: int, stride: int, group=None, storage=None
     return torch.cat([p[1] for p in pieces], dim=0)
 
 
-def exclusive_scan_over_ranks(vec, add, group=None):
-    """All-gather per-rank vectors and return (sum of lower ranks' vectors, sum of all)."""
+def gather_over_ranks(vec, group=None):
+    """All-gather every rank's (len,) vector into one (n, len) tensor (rank order)."""
     import torch
 
     dist = _dist()
     rank, n = world(group)
+    vec = vec.contiguous()
     if n == 1:
-        return None, vec
+        return vec.unsqueeze(0)
+    if vec.is_cuda:  # NCCL: one collective straight into the stacked buffer
+        out = torch.empty((n,) + tuple(vec.shape), dtype=vec.dtype, device=vec.device)
+        dist.all_gather_into_tensor(out, vec, group)
+        return out
     parts = [torch.empty_like(vec) for _ in range(n)]
-    dist.all_gather(parts, vec.contiguous(), group)
-    carry = None
-    for g in range(rank):
-        carry = parts[g].clone() if carry is None else add(carry, parts[g])
-    total = None
-    for p in parts:
-        total = p.clone() if total is None else add(total, p)
-    return carry, total
+    dist.all_gather(parts, vec, group)
+    return torch.stack(parts)
+
+
+def exclusive_scan_over_ranks(vec, backend, group=None):
+    """(sum of lower ranks' vectors, or None on rank 0) -- the carry row of this
+    rank's band: the exclusive scan over bands of their column-total vectors,
+    summed in rank order by ``backend.carry`` (a kernel on the CUDA backend)."""
+    rank, n = world(group)
+    if n == 1 or rank == 0:
+        if n > 1:
+            gather_over_ranks(vec, group)  # every rank takes part in the collective
+        return None
+    return backend.carry(gather_over_ranks(vec, group), rank)
 
 
 # ----------------------------------------------------------------------------- backends
 class CudaBackend:
-    """Local compute through libsatsweep_b200.so on this rank's device."""
+    """Local compute through libsatsweep_b200.so on this rank's device.
+
+    Buffers (workspace, totals, band table, outputs) are allocated on first
+    use and reused by later calls of the same shape, so a repeated step
+    (bench.py) allocates nothing."""
 
     def __init__(self, device=None):
         from . import _device
 
         self.device = device or _device.current_device()
+        self._bufs: dict = {}
+        self._side = None
 
-    def window(self, x, kind: ElemKind, w: int, stride: int, stats, pipeline: str = "auto"):
+    def _buf(self, key, shape, np_dtype, what):
+        from . import _device
+
+        cur = self._bufs.get(key)
+        if cur is None or tuple(cur.shape) != tuple(shape) or cur.dtype != _device.storage_dtype(np_dtype):
+            self._bufs.pop(key, None)
+            cur = _device.empty(shape, np_dtype, self.device, what)
+            self._bufs[key] = cur
+        return cur
+
+    def _outs(self, kind: ElemKind, stats, out_r: int, out_c: int):
+        from . import _engine
+
+        return {s: self._buf(("out", s), (out_r, out_c), _engine.result_dtype(kind, s), "band result") for s in stats}
+
+    def window(self, x, kind: ElemKind, w: int, stride: int, stats, pipeline: str = "auto", outs=None):
         from . import _engine
         from .grid import ImageGrid
 
         img = ImageGrid(x, kind)
-        return _engine.run_device(img, w, stride, list(stats), pipeline)
+        return _engine.run_device(img, w, stride, list(stats), pipeline, outs=outs)
+
+    def window_start(self, x, kind: ElemKind, w: int, stats):
+        """Stride-1 window stats of ``x`` into reused outputs, on a side stream
+        forked from the current one (overlaps the table phases); window_finish joins."""
+        torch = __import__("torch")
+        rows, cols = int(x.shape[0]), int(x.shape[1])
+        outs = self._outs(kind, list(stats), rows - w + 1, cols - w + 1)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        cur = torch.cuda.current_stream(self.device)
+        self._side.wait_stream(cur)
+        with torch.cuda.stream(self._side):
+            pipe = "fused" if w <= _fused_max_w() else "table"
+            res = self.window(x, kind, w, 1, stats, pipe, outs=outs)
+        return res
+
+    def window_finish(self, handle):
+        torch = __import__("torch")
+        torch.cuda.current_stream(self.device).wait_stream(self._side)
+        return handle
 
     def band_totals(self, x, kind: ElemKind, squared: bool):
-        import ctypes
-
-        from . import _device, _engine, _lib
+        from . import _device, _lib
 
         lib = _lib.load()
         rows, cols = int(x.shape[0]), int(x.shape[1])
         acc = np.float64 if kind is ElemKind.F32 else np.uint64
         ws_bytes = int(lib.ssb_sat_workspace_bytes(kind.abi_code, rows, cols, 1 if squared else 0))
-        ws = _device.empty((max(ws_bytes, 8),), np.uint8, self.device, "table workspace")
-        tot = _device.empty((cols + 1,), acc, self.device, "band totals")
-        tot_sq = _device.empty((cols + 1,), acc, self.device, "band totals") if squared else None
+        ws = self._buf("ws", (max(ws_bytes, 8),), np.uint8, "table workspace")
+        tot = self._buf("tot", (cols + 1,), acc, "band totals")
+        tot_sq = self._buf("tot_sq", (cols + 1,), acc, "band totals") if squared else None
         rc = lib.ssb_sat_prepare(x.data_ptr(), kind.abi_code, rows, cols, cols, 1 if squared else 0, ws.data_ptr(),
                                  ws_bytes, tot.data_ptr(), None if tot_sq is None else tot_sq.data_ptr(), None,
                                  _device.stream_ptr(self.device))
         _lib.check(rc, "band totals")
-        del ctypes, _engine
-        return {"ws": ws, "ws_bytes": ws_bytes, "tot": tot, "tot_sq": tot_sq}
+        return {"ws": ws, "ws_bytes": ws_bytes, "tot": None if squared else tot, "tot_sq": tot_sq}
 
-    def add(self, a, b):
-        return a + b  # int64 storage wraps like uint64; float64 adds
+    def carry(self, gathered, rank: int):
+        """Sum of rows [0, rank) of the gathered (n, len) totals, in row order (ssb_band_carry)."""
+        from . import _device, _lib
+
+        lib = _lib.load()
+        length = int(gathered.shape[1])
+        out = self._buf(("carry", gathered.dtype), (length,), np.float64 if gathered.dtype == _device.torch().float64
+                        else np.uint64, "carry row")
+        is_float = 1 if gathered.dtype == _device.torch().float64 else 0
+        _lib.check(lib.ssb_band_carry(gathered.data_ptr(), rank, length, length, is_float, out.data_ptr(),
+                                      _device.stream_ptr(gathered.device)), "band carry")
+        return out
 
     def finish(self, x, kind: ElemKind, state, carry, carry_sq, squared: bool):
         from . import _device, _engine, _lib
@@ -233,14 +297,19 @@ class CudaBackend:
         rows, cols = int(x.shape[0]), int(x.shape[1])
         ld = _engine.sat_ld_for(cols)
         acc = np.float64 if kind is ElemKind.F32 else np.uint64
-        sat = None if squared else _device.empty((rows + 1, ld), acc, self.device, "band table")
-        sq = _device.empty((rows + 1, ld), acc, self.device, "band table") if squared else None
+        tab = self._buf(("table", squared), (rows + 1, ld), acc, "band table")
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-        rc = lib.ssb_sat_finish(x.data_ptr(), kind.abi_code, rows, cols, cols, ptr(sat), ptr(sq), ld, ptr(carry),
-                                ptr(carry_sq), state["ws"].data_ptr(), state["ws_bytes"],
-                                _device.stream_ptr(self.device))
+        rc = lib.ssb_sat_finish(x.data_ptr(), kind.abi_code, rows, cols, cols, None if squared else ptr(tab),
+                                ptr(tab) if squared else None, ld, ptr(carry), ptr(carry_sq), state["ws"].data_ptr(),
+                                state["ws_bytes"], _device.stream_ptr(self.device))
         _lib.check(rc, "band table")
-        return (sq if squared else sat), ld
+        return tab, ld
+
+
+def _fused_max_w() -> int:
+    from . import _engine
+
+    return _engine.fused_max_w()
 
 
 # ----------------------------------------------------------------------------- entry points
@@ -278,6 +347,40 @@ def build_sat_sharded(band, rows: int, cols: int, kind: ElemKind, squared: bool 
     assert band.shape[0] == b - a
     state = backend.band_totals(band, kind, squared)
     mine = state["tot_sq"] if squared else state["tot"]
-    carry, _ = exclusive_scan_over_ranks(mine, backend.add, group)
+    carry = exclusive_scan_over_ranks(mine, backend, group)
     table, ld = backend.finish(band, kind, state, None if squared else carry, carry if squared else None, squared)
     return ShardedResult((a, b), {"table": table}, ld)
+
+
+def swa_table_sharded(band, rows: int, cols: int, kind: ElemKind, w: int, stats=(StatKind.SUM,), backend=None,
+                      group=None, storage=None):
+    """The multi-GPU step of bench.py: the stride-1 window statistics of this
+    rank's output band AND the global integral-image rows of its owned band.
+
+    ``band`` holds the rows ``window_input_bands`` assigns to this rank (the
+    owned-rows view of ``storage`` for the zero-copy halo).  The halo arrives by
+    P2P, the windows run on a side stream (``backend.window_start``) while the
+    table phases run on the current one: band column totals -> all-gather ->
+    exclusive scan over ranks (the carry row) -> table rows written with the
+    carry.  Returns (window result, table result); the table result holds
+    global table rows [a_g, b_g] of the owned rows [a_g, b_g)."""
+    rank, n = world(group)
+    backend = backend or CudaBackend()
+    x = halo_exchange(band, rows, w, 1, group, storage=storage)
+    lo, hi = output_partition(rows - w + 1, n)[rank]
+    a, b = window_input_bands(rows, w, 1, n)[rank]
+    assert band.shape[0] == b - a
+    handle = backend.window_start(x, kind, w, stats) if hi > lo else None
+    if b > a:
+        state = backend.band_totals(band, kind, False)
+        carry = exclusive_scan_over_ranks(state["tot"], backend, group)
+        table, ld = backend.finish(band, kind, state, carry, None, False)
+    else:  # an empty band still joins the collective; its table is the carry row
+        import torch
+
+        acc = torch.float64 if kind is ElemKind.F32 else torch.int64
+        zero = torch.zeros(cols + 1, dtype=acc, device=getattr(band, "device", None))
+        carry = exclusive_scan_over_ranks(zero, backend, group)
+        table, ld = (zero if carry is None else carry).unsqueeze(0).clone(), cols + 1
+    vals = backend.window_finish(handle) if handle is not None else {}
+    return ShardedResult((lo, hi), vals), ShardedResult((a, b), {"table": table}, ld)

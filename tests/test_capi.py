@@ -82,3 +82,32 @@ def test_table_and_windows_contract(lib):
         assert rc == _lib.EUNSUPPORTED
         rc = fn(None, _lib.U8, 8, 8, 8, None, 10, 9, _lib.SUM, None, None, 6, None, 0, None)
         assert rc == _lib.EINVAL and b"exceeds grid dims" in lib.ssb_last_error()
+
+
+@pytest.mark.parametrize("rows,w,n", [(100, 7, 4), (9, 9, 3), (12, 11, 3), (70000, 256, 8), (5, 1, 8), (61, 9, 2)])
+def test_sharded_plan_matches_host_geometry(lib, rows, w, n):
+    """ssb_sharded_plan (pure host) == shard.py's geometry (the reference's partition
+    rule over output rows, parallel.py:80-90): owned rows partition [0, rows);
+    the needed rows are the band plus its (w-1)-row halo."""
+    from paper_2410_16291_b200 import shard
+
+    buf = (ctypes.c_int64 * (7 * n))()
+    assert lib.ssb_sharded_plan(rows, 40 if w <= 40 else w, w, n, buf) == 0
+    v = list(buf)
+    own = shard.window_input_bands(rows, w, 1, n)
+    need = shard.window_needed_rows(rows, w, 1, n)
+    out = shard.output_partition(rows - w + 1, n)
+    for g in range(n):
+        own_lo, own_hi, need_lo, need_hi, out_lo, out_hi, cap = v[7 * g:7 * g + 7]
+        assert (own_lo, own_hi) == own[g]
+        assert (out_lo, out_hi) == out[g]
+        if out_hi > out_lo:
+            assert (need_lo, need_hi) == need[g]
+            assert cap >= need_hi - own_lo
+        assert cap >= own_hi - own_lo
+
+
+def test_sharded_validation_without_device(lib):
+    assert lib.ssb_sharded_plan(10, 10, 11, 2, (ctypes.c_int64 * 14)()) == _lib.EINVAL
+    assert lib.ssb_sharded_workspace_bytes(_lib.U8, 10, 10, 3, 2, 5, 1) == -1
+    assert lib.ssb_band_carry(None, 1, 10, 10, 0, None, None) == _lib.EINVAL

@@ -36,6 +36,12 @@ class NumpyBackend:
             out[s] = torch.from_numpy(r.view(np.int64) if r.dtype == np.uint64 else r)
         return out
 
+    def window_start(self, x, kind, w, stats):
+        return self.window(x, kind, w, 1, stats)
+
+    def window_finish(self, handle):
+        return handle
+
     def band_totals(self, x, kind, squared):
         import torch
 
@@ -47,12 +53,13 @@ class NumpyBackend:
         tot = torch.from_numpy(last.view(np.int64) if last.dtype == np.uint64 else last.copy())
         return {"tot": None if squared else tot, "tot_sq": tot if squared else None, "x": a}
 
-    def add(self, a, b):
+    def carry(self, gathered, rank):
         import torch
 
-        if a.dtype == torch.float64:
-            return a + b
-        return torch.from_numpy((a.numpy().view(np.uint64) + b.numpy().view(np.uint64)).view(np.int64))
+        g = gathered.numpy()
+        if g.dtype == np.float64:
+            return torch.from_numpy(g[:rank].sum(axis=0))
+        return torch.from_numpy(g.view(np.uint64)[:rank].sum(axis=0, dtype=np.uint64).view(np.int64))
 
     def finish(self, x, kind, state, carry, carry_sq, squared):
         import torch
@@ -99,7 +106,16 @@ def _worker(rank, world, port, img, w, stride, q):
             assert np.array_equal(v.numpy(), win[k.value]), k
         a, b = shard.table_input_bands(rows, world)[rank]
         tab = shard.build_sat_sharded(torch.from_numpy(img[a:b].copy()), rows, cols, kind, backend=NumpyBackend())
-        q.put((rank, res.rows, win, tab.rows, tab.values["table"].numpy()))
+        # the combined step (bench.py at N > 1): windows of the output band and
+        # global table rows of the OWNED window band, in one call
+        comb = None
+        if stride == 1:
+            a, b = shard.window_input_bands(rows, w, 1, world)[rank]
+            wr, tr = shard.swa_table_sharded(torch.from_numpy(img[a:b].copy()), rows, cols, kind, w,
+                                             (StatKind.SUM,), backend=NumpyBackend())
+            comb = (wr.rows, {k.value: v.numpy() for k, v in wr.values.items()}, tr.rows,
+                    tr.values["table"].numpy())
+        q.put((rank, res.rows, win, tab.rows, tab.values["table"].numpy(), comb))
     finally:
         dist.destroy_process_group()
 
@@ -120,7 +136,8 @@ def run(world, img, w, stride):
     return sorted(out, key=lambda r: r[0])
 
 
-@pytest.mark.parametrize("world,shape,w,stride", [(2, (61, 37), 9, 1), (3, (50, 23), 17, 2), (2, (12, 40), 11, 1)])
+@pytest.mark.parametrize("world,shape,w,stride",
+                         [(2, (61, 37), 9, 1), (3, (50, 23), 17, 2), (2, (12, 40), 11, 1), (3, (12, 40), 11, 1)])
 def test_sharded_matches_whole_image(world, shape, w, stride):
     from oracle import satsweep_oracle as O
 
@@ -134,8 +151,15 @@ def test_sharded_matches_whole_image(world, shape, w, stride):
     np.testing.assert_array_equal(means, O.swa(img, w, "mean", stride))
     # table path: rank g holds global table rows [a_g, a_{g+1}]
     full = O.build_table(img)
-    for rank, _, _, (a, b), table in parts:
+    for rank, _, _, (a, b), table, _ in parts:
         np.testing.assert_array_equal(table.view(np.uint64), full[a:b + 1])
+    if stride == 1:
+        combs = [p[5] for p in parts]
+        sums2 = np.concatenate([c[1]["sum"] for c in combs if c[1]], axis=0).view(np.uint64)
+        np.testing.assert_array_equal(sums2, O.swa(img, w, "sum"))
+        assert combs[0][2][0] == 0 and combs[-1][2][1] == img.shape[0]
+        for (_, _, (a, b), table) in combs:
+            np.testing.assert_array_equal(table.view(np.uint64)[:, : img.shape[1] + 1], full[a:b + 1])
 
 
 def test_geometry_helpers():
