@@ -2,28 +2,29 @@
 
 Workload (BASELINE.json `metric`, configs[4] = C5): a 70,000 x 85,000 uint8
 binary mask (5.95 Gpx; seeded synthetic stand-in, paper_2410_16291_b200/synthetic.py),
-integral image (uint64/int64) + window sum w=256 stride 1 (69,745 x 84,745
+its integral image (uint64) AND the window sums w=256 stride 1 (69,745 x 84,745
 uint64 outputs).  One step = one pass of the hot path over the whole image:
 
-  headline `value`: the launches of ssb_sat_build_swa -- ssb_sat_build (the
-  integral image written to HBM) then ssb_window_fused (the window sums,
-  evaluated from the raster instead of reading the table back).  Same table
-  and same outputs as the reference's build_sat + sweep_window_sums
-  (pkg/src/satsweep/integral.py:109-116, :141-163).  Also reported: the
-  corner-sweep table pipeline (ssb_sat_build -> ssb_window_eval, the
-  reference's structure), the one-pass kernel (ssb_sat_build_swa_onepass),
-  and the fused window sums alone (no table).
+  N = 1: one ssb_sat_build_swa call -- the table build (ssb_sat_build) on the
+  step's stream and, concurrently on a forked stream, the window sums from the
+  raster (ssb_window_fused); same table and same outputs as the reference's
+  build_sat + sweep_window_sums (pkg/src/satsweep/integral.py:109-116, :141-163).
+  N > 1 (one rank per GPU): rank g owns a row band; the (w-1)-row halo arrives
+  over NCCL P2P, the band's windows run on a side stream, and the GLOBAL table
+  rows of the band are written with the carry row from an NCCL all-gather +
+  exclusive scan of the bands' column totals (shard.swa_table_sharded) -- the
+  same products as at N = 1, strong scaling of the fixed image.
 
 `value` is device-resident throughput (input already in HBM, outputs
-preallocated, inputs 5.95 GB >> 126 MB L2, so no flush is needed); `e2e` runs
+preallocated; inputs 5.95 GB >> 126 MB L2, so no flush is needed); `e2e` runs
 the public API with pinned host buffers (host->device input copy and
 device->host result copy inside every timed step).  `--impl reference` times
-the reference algorithm (the numpy port under oracle/, all host threads) on a
-bounded band of the same workload.
+the reference itself (`satsweep` installed under baseline/_ref, its
+bench.run_timed("parallel") on all host cores) on a bounded band of the same
+workload; `configs` holds C1-C4 through the public API (device-resident).
 
-Multi-GPU: `python -m torch.distributed.run --nproc-per-node N bench.py --gpus N`
-shards output rows across ranks (strong scaling of the fixed image); each rank
-receives its (w-1)-row halo over NCCL inside the timed step.
+`python bench.py --gpus N` relaunches itself under torch.distributed.run with N
+ranks when WORLD_SIZE is not set.
 """
 
 from __future__ import annotations
@@ -31,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,8 +46,10 @@ REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 ROWS, COLS, W = 70000, 85000, 256
+OUT_R, OUT_C = ROWS - W + 1, COLS - W + 1
 METRIC = "Gpixels/s (integral image + window sum) at 70k×85k; % HBM roofline; 1/2/4/8 GPU"
 UNIT = "Gpixels/s"
+WORKLOAD = "C5 70000x85000 u8 mask, integral image (u64) + window sum w=256 stride 1"
 
 
 def peaks() -> dict:
@@ -111,6 +115,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "power_w_max": max(r[2] for r in rows)}
 
 
+
+
 # ----------------------------------------------------------------------------- helpers
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
@@ -123,50 +129,191 @@ def emit(obj: dict) -> None:
     print(json.dumps(obj), flush=True)
 
 
-_BANDS: dict = {}
+def relaunch(n: int) -> int:
+    """Re-run this script as N ranks (one per GPU) under torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
-def cpu_port_band(out_rows: int, threads: int = 0):
-    """Reference algorithm (oracle port) on output rows [0, out_rows) of C5; returns (seconds, pixels).
+# ----------------------------------------------------------------------------- CPU reference
+class Reference:
+    """The reference implementation on the host cores.
 
-    The band is generated once per size (untimed) and reused across steps."""
-    from oracle import satsweep_oracle as oracle
-    from paper_2410_16291_b200 import synthetic
+    Preferred: the reference package itself, installed unmodified under
+    baseline/_ref (`pip install --target baseline/_ref`), called through its
+    own benchmark entry point satsweep.bench.run_timed (bench.py:79-105), which
+    times the build and query phases of swa_parallel (all os.cpu_count()
+    workers, parallel.py:71-72) or the sequential swa_integral.  If it is not
+    installed, the numpy restatement oracle/satsweep_oracle.swa_threaded stands
+    in (kind "port")."""
 
-    if out_rows not in _BANDS:
-        _BANDS[out_rows] = synthetic.c5(0, out_rows + W - 1)
-    band = _BANDS[out_rows]
-    t0 = time.perf_counter()
-    res = oracle.swa_threaded(band, W, "sum", 1, threads or (os.cpu_count() or 1))
-    dt = time.perf_counter() - t0
-    del res
-    # pixel credit: the band's own output rows' share of the image (halo rows are overhead)
-    return dt, out_rows * COLS
+    def __init__(self):
+        self.kind = "port"
+        self.mod = None
+        ref = REPO / "baseline" / "_ref"
+        if (ref / "satsweep" / "bench.py").exists():
+            sys.path.insert(0, str(ref))
+            import satsweep
+            import satsweep.bench
+
+            if Path(satsweep.__file__).resolve().is_relative_to(ref.resolve()):
+                self.mod = satsweep
+                self.kind = "reference"
+        self._bands: dict = {}
+
+    def band(self, out_rows: int) -> np.ndarray:
+        """Input rows of C5 output rows [0, out_rows) (generated once, untimed)."""
+        from paper_2410_16291_b200 import synthetic
+
+        if out_rows not in self._bands:
+            self._bands[out_rows] = synthetic.c5(0, out_rows + W - 1, threads=os.cpu_count() or 1)
+        return self._bands[out_rows]
+
+    def run(self, out_rows: int, method: str = "parallel") -> dict:
+        """One timed run on a band; returns seconds (build/query split when the reference runs)."""
+        band = self.band(out_rows)
+        if self.mod is not None:
+            sb = self.mod
+            img = sb.ImageGrid(band)
+            r = sb.bench.run_timed(method, img, sb.WindowSpec(W), sb.StatKind.SUM, threads=0)
+            res = {"s": r.total_s, "build_s": r.build_s, "query_s": r.query_s, "workers": r.workers}
+            del r
+            return res
+        from oracle import satsweep_oracle as oracle
+
+        t0 = time.perf_counter()
+        out = oracle.swa_threaded(band, W, "sum", 1, (os.cpu_count() or 1) if method == "parallel" else 1)
+        dt = time.perf_counter() - t0
+        del out
+        return {"s": dt, "workers": (os.cpu_count() or 1) if method == "parallel" else 1}
+
+    @staticmethod
+    def pixels(out_rows: int) -> float:
+        """Pixel credit of a band: its share of the image's output rows x the image's pixels."""
+        return out_rows / OUT_R * ROWS * COLS
+
+    def describe(self) -> str:
+        if self.kind == "reference":
+            return "satsweep (the reference, baseline/_ref) bench.run_timed"
+        return "oracle/satsweep_oracle.swa_threaded (numpy restatement of satsweep.swa_parallel)"
 
 
-# ----------------------------------------------------------------------------- reference arm
+def cores() -> dict:
+    try:
+        import psutil
+
+        phys = psutil.cpu_count(logical=False)
+    except Exception:  # pragma: no cover
+        phys = None
+    return {"logical": os.cpu_count(), "physical": phys}
+
+
 def run_reference(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
+    ref = Reference()
     out_rows = args.ref_rows
+    ref.band(out_rows)
     times = []
     for i in range(args.warmup + args.steps):
-        dt, px = cpu_port_band(out_rows, threads)
+        r = ref.run(out_rows, "parallel")
         if i >= args.warmup:
-            times.append(dt)
-    t = sum(times) / len(times)
-    v = px / t / 1e9
-    sample = (f"C5 band of {out_rows} output rows x {COLS} cols ({out_rows + W - 1} input rows) per step; "
-              f"oracle/satsweep_oracle.swa_threaded (numpy restatement of satsweep.swa_parallel)")
+            times.append(r["s"])
+    t = statistics.median(times)
+    v = ref.pixels(out_rows) / t / 1e9
+    c = cores()
+    sample = (f"C5 output rows [0, {out_rows}) ({out_rows + W - 1} input rows x {COLS} cols) per step, credited "
+              f"{out_rows}/{OUT_R} of the image's {ROWS * COLS} px; {ref.describe()}('parallel', threads=0 -> "
+              f"{c['logical']} workers); value from the median step")
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
           "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded C5 recipe)",
-          "config": {"workload": "C5 70000x85000 u8, integral image + window sum w=256 stride 1",
-                     "sample_rows": out_rows},
-          "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+          "config": {"workload": WORKLOAD, "sample_rows": out_rows},
+          "step_s": times,
+          "cpu_baseline": {"value": v, "unit": UNIT, "cores": c["logical"], "physical_cores": c["physical"],
+                           "kind": ref.kind, "sample": sample},
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+def cpu_baseline(args) -> dict:
+    """The reference on a bounded sample (rank 0, N = 1): median of 3 parallel
+    runs on all host cores plus one single-thread run ("integral")."""
+    ref = Reference()
+    par = [ref.run(args.cpu_rows, "parallel") for _ in range(max(1, args.cpu_reps))]
+    t = statistics.median(r["s"] for r in par)
+    seq = ref.run(args.cpu_rows_seq, "integral")
+    c = cores()
+    return {"value": ref.pixels(args.cpu_rows) / t / 1e9, "unit": UNIT, "cores": c["logical"],
+            "physical_cores": c["physical"], "kind": ref.kind,
+            "sample": (f"median of {len(par)} runs of {ref.describe()}('parallel', threads=0) on C5 output rows "
+                       f"[0, {args.cpu_rows}) ({args.cpu_rows + W - 1} input rows), credited {args.cpu_rows}/{OUT_R} "
+                       f"of the image"),
+            "runs_s": [r["s"] for r in par],
+            "build_query_s": [[r.get("build_s"), r.get("query_s")] for r in par],
+            "single_thread": {"value": ref.pixels(args.cpu_rows_seq) / seq["s"] / 1e9, "unit": UNIT, "cores": 1,
+                              "method": "integral", "sample_rows": args.cpu_rows_seq, "s": seq["s"],
+                              "build_s": seq.get("build_s"), "query_s": seq.get("query_s")}}
+
+
+# ----------------------------------------------------------------------------- C1-C4 through the public API
+def run_configs(args, dev, pk) -> dict:
+    """BASELINE configs C1-C4, device-resident, through the public API (auto
+    pipelines), K timed calls each bracketed by CUDA events on the API's stream."""
+    import torch
+
+    import paper_2410_16291_b200 as sb
+    from paper_2410_16291_b200 import _lib, synthetic
+
+    res = {}
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, steps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        l0 = _lib.launch_count()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b) / steps, (_lib.launch_count() - l0) / steps
+
+    cases = [
+        ("C1", "2048x2048 u8 Bernoulli(0.05), sum w=50", synthetic.c1, lambda x: sb.swa(x, 50, "sum"),
+         lambda r, c: r * c + (r - 49) * (c - 49) * 8),
+        ("C2", "10000x10000 int32 Thomas counts, sum + mean w=100", synthetic.c2,
+         lambda x: sb.swa_stats(x, 100, ("sum", "mean")), lambda r, c: r * c * 4 + 2 * (r - 99) * (c - 99) * 8),
+        ("C3", "30000x30000 u8 mask, sums for w in 25/50/100/200/400 from one table", synthetic.c3,
+         lambda x: sb.multi_window(x, [25, 50, 100, 200, 400], "sum"),
+         lambda r, c: r * c + sum((r - w + 1) * (c - w + 1) * 8 for w in (25, 50, 100, 200, 400))),
+        ("C4", "20000x24000 f32 lognormal, mean + std w=64 (fp64)", synthetic.c4,
+         lambda x: sb.swa_stats(x, 64, ("mean", "std")), lambda r, c: r * c * 4 + 2 * (r - 63) * (c - 63) * 8),
+    ]
+    for name, desc, gen, call, floor in cases:
+        try:
+            host = gen()
+            x = torch.from_numpy(host).to(dev)
+            r, c = host.shape
+            del host
+            steps = 20 if name == "C1" else max(3, args.steps // 2)
+            ms, launches = timed(lambda: call(x), steps)
+            fb = floor(r, c)
+            res[name] = {"workload": desc, "ms_per_call": ms, "gpx_s": r * c / (ms * 1e-3) / 1e9, "steps": steps,
+                         "floor_bytes": fb, "floor_frac": fb / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                         "launches_per_call": launches,
+                         "floor": "input read once + every output written once (the fused-pipeline floor, SURVEY 8d)"}
+            del x
+            sb.release_scratch()
+        except Exception as exc:  # pragma: no cover - reporting only
+            res[name] = {"error": repr(exc)}
+    return res
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -176,100 +323,83 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--ref-rows", type=int, default=16384, help="output rows per reference/CPU step")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-rows", type=int, default=16384, help="output rows per reference step (bounded sample)")
     ap.add_argument("--cpu-rows", type=int, default=16384, help="output rows of the cpu_baseline sample")
-    ap.add_argument("--cpu-reps", type=int, default=8, help="repetitions of the cpu_baseline sample (~10-30 s of CPU work)")
+    ap.add_argument("--cpu-rows-seq", type=int, default=4096, help="output rows of the single-thread sample")
+    ap.add_argument("--cpu-reps", type=int, default=3, help="parallel runs of the cpu_baseline sample (median)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--rows", type=int, default=ROWS, help="(debug) smaller image")
+    ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other pipelines' lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
 
     import torch
 
-    from paper_2410_16291_b200 import _device, _engine, _lib, shard, synthetic
+    from paper_2410_16291_b200 import _device, _lib, shard, synthetic
     from paper_2410_16291_b200.grid import ElemKind, StatKind
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    group = None
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
-    rows = args.rows
     kind = ElemKind.U8
+    pk = peaks()
 
     # ---- inputs: this rank's owned rows, generated on the host, copied once (untimed)
-    a_own, b_own = shard.window_input_bands(rows, W, 1, world)[rank]
+    a_own, b_own = shard.window_input_bands(ROWS, W, 1, world)[rank]
     t_gen = time.perf_counter()
-    host_band = synthetic.c5(a_own, b_own) if rows == ROWS else synthetic.bernoulli_rows(5, rows, COLS, 0.01, a_own, b_own)
+    host_band = synthetic.c5(a_own, b_own, threads=os.cpu_count() or 1)
     gen_s = time.perf_counter() - t_gen
     # zero-copy halo layout: the band lives at the head of a buffer with room
     # for its halo, which NCCL receives in place each step (no concatenation)
-    storage, x_own = shard.band_storage(rows, COLS, W, 1, torch.uint8, dev)
+    storage, x_own = shard.band_storage(ROWS, COLS, W, 1, torch.uint8, dev)
     x_own.copy_(torch.from_numpy(host_band))
     del host_band
-    need = shard.window_needed_rows(rows, W, 1, world)[rank]
+    need = shard.window_needed_rows(ROWS, W, 1, world)[rank]
     nr = need[1] - need[0]
-    out_lo, out_hi = shard.output_partition(rows - W + 1, world)[rank]
+    own_r = b_own - a_own
+    out_lo, out_hi = shard.output_partition(OUT_R, world)[rank]
     n_out = out_hi - out_lo
-    out_c = COLS - W + 1
-    ld = _engine.sat_ld_for(COLS)
-    sat = _device.empty((nr + 1, ld), np.uint64, dev, "table")
-    out = _device.empty((n_out, out_c), np.uint64, dev, "result")
-    ws_bytes = max(int(lib.ssb_sat_workspace_bytes(kind.abi_code, nr, COLS, 0)),
-                   int(lib.ssb_sat_swa_workspace_bytes(kind.abi_code, nr, COLS)))
-    ws = _device.empty((ws_bytes,), np.uint8, dev, "workspace")
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
-    def get_x():
-        if world == 1:
-            return x_own
-        return shard.halo_exchange(x_own, rows, W, 1, group, storage=storage)
+    from paper_2410_16291_b200 import _engine
 
-    ev = {k: [] for k in ("build", "windows", "group", "group_phase")}
+    ld = _engine.sat_ld_for(COLS)
+    if world == 1:
+        sat = _device.empty((ROWS + 1, ld), np.uint64, dev, "table")
+        out = _device.empty((OUT_R, OUT_C), np.uint64, dev, "result")
+        ws_bytes = max(int(lib.ssb_sat_workspace_bytes(kind.abi_code, ROWS, COLS, 0)),
+                       int(lib.ssb_sat_swa_workspace_bytes(kind.abi_code, ROWS, COLS)))
+        ws = _device.empty((ws_bytes,), np.uint8, dev, "workspace")
 
-    side = torch.cuda.Stream(dev)
+        def step():
+            # the timed step: one ssb_sat_build_swa call -- the table build on
+            # this stream and, concurrently on the library's forked side stream,
+            # the window sums from the raster, joined back before it returns
+            _lib.check(lib.ssb_sat_build_swa(x_own.data_ptr(), kind.abi_code, ROWS, COLS, COLS, sat.data_ptr(), ld,
+                                             W, _lib.SUM, out.data_ptr(), None, OUT_C, ws.data_ptr(), ws_bytes, sptr))
+    else:
+        backend = shard.CudaBackend(dev)
 
-    def step(record: bool):
-        # the timed step: one ssb_sat_build_swa call -- the table build
-        # (reduce-then-scan; SSB_SAT_PATH=one selects the single-pass look-back
-        # kernel) on this stream and, concurrently on the library's forked side
-        # stream, the window sums from the raster, joined back before it returns
-        # (the step's duration is the group's: start/stop events bracket the loop)
-        x = get_x()
-        _lib.check(lib.ssb_sat_build_swa(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), ld, W, _lib.SUM,
-                                         out.data_ptr(), None, out_c, ws.data_ptr(), ws_bytes, sptr))
-
-    def phase_step(record: bool):
-        # the same launches issued from here with an event around each kernel
-        # group (per-kernel times in context; not the timed step)
-        x = get_x()
-        e0, e1, f0, f1, ej = (torch.cuda.Event(enable_timing=True) for _ in range(5))
-        e0.record(stream)
-        side.wait_event(e0)
-        _lib.check(lib.ssb_sat_build(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), None, ld, None,
-                                     None, ws.data_ptr(), ws_bytes, None, sptr))
-        e1.record(stream)
-        f0.record(side)
-        _lib.check(lib.ssb_window_fused(x.data_ptr(), kind.abi_code, nr, COLS, COLS, W, _lib.SUM, out.data_ptr(),
-                                        None, None, out_c, None, 0, side.cuda_stream))
-        f1.record(side)
-        stream.wait_event(f1)
-        ej.record(stream)
-        if record:
-            ev["build"].append((e0, e1))
-            ev["windows"].append((f0, f1))
-            ev["group_phase"].append((e0, ej))
+        def step():
+            # the timed step at N > 1: halo (NCCL P2P) -> windows on a side
+            # stream || band totals -> NCCL all-gather -> carry -> global table rows
+            shard.swa_table_sharded(x_own, ROWS, COLS, kind, W, (StatKind.SUM,), backend, storage=storage)
 
     def barrier():
         if world > 1:
@@ -279,7 +409,7 @@ def main() -> None:
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        step(False)
+        step()
     barrier()
     launches0 = _lib.launch_count()
     start = torch.cuda.Event(enable_timing=True)
@@ -288,162 +418,145 @@ def main() -> None:
         barrier()
         start.record(stream)
         for _ in range(args.steps):
-            step(True)
+            step()
         stop.record(stream)
         barrier()
     launches = _lib.launch_count() - launches0
     ms_total = start.elapsed_time(stop)
-    for i in range(args.warmup + args.steps):  # per-kernel phases of the same step (untimed pass)
-        phase_step(i >= args.warmup)
     if world > 1:
         import torch.distributed as dist
 
         t = torch.tensor([ms_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
+        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
     ms_step = ms_total / args.steps
-    barrier()
-    phase_ms = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in ev.items() if v}
-    phase_ms["group_phase_pass"] = phase_ms.pop("group_phase")
-    phase_ms["group"] = ms_step  # the timed step is exactly the group (one ssb_sat_build_swa call)
 
-    # ---- algorithmic bytes: in + table write | table read + out write
-    px_in = nr * COLS
-    tab_bytes = (nr + 1) * (COLS + 1) * 8
-    out_bytes = n_out * out_c * 8
-    # the step's two kernel groups run concurrently, so the roofline is taken on
-    # the group: each kernel's algorithmic bytes (sat_build: image read + table
-    # write; window_fused: image read + window sums write) over the group's
-    # duration (fork event -> join event on the step's stream)
-    kernels = {
-        "sat_build (image read + table write)": (px_in + tab_bytes, phase_ms["build"]),
-        "window_fused (image read + window sums write)": (px_in + out_bytes, phase_ms["windows"]),
-    }
-    pk = peaks()
-    dom = "sat_build || window_fused (concurrent kernel group of one step)"
-    dom_bytes, dom_ms = sum(b for b, _ in kernels.values()), phase_ms["group"]
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    # ---- algorithmic bytes: the image read once, the table and
+    # the window sums written once (17 B/px at C5)
+    px = ROWS * COLS
+    tab_bytes = (ROWS + 1) * (COLS + 1) * 8
+    out_bytes = OUT_R * OUT_C * 8
+    b_alg = px + tab_bytes + out_bytes
+    b_mat = px + 2 * tab_bytes + out_bytes  # the reference structure (table written, then read back)
+    value = px / (ms_step * 1e-3) / 1e9
+    achieved = b_alg / (ms_step * 1e-3) / 1e9
+    peak_all = pk["hbm_gbs"] * world
     traffic = None
     tfile = REPO / "profiles" / "traffic.json"
     if tfile.exists():
         tr = json.loads(tfile.read_text())
-        if "sat_build" in tr and "window_fused" in tr:
-            traffic = tr["sat_build"] + tr["window_fused"]
-    b_alg = px_in + tab_bytes + out_bytes  # every distinct array read or written once
-    b_mat = px_in + 2 * tab_bytes + out_bytes  # the reference structure (table written, then read back)
-    value = rows * COLS / (ms_step * 1e-3) / 1e9
-
+        traffic = tr.get("step_total")
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded C5 recipe, synthetic.py)",
-        "config": {"workload": "C5 70000x85000 u8 mask, integral image (u64) + window sum w=256 stride 1",
-                   "pipeline": "table + windows: ssb_sat_build_swa (ssb_sat_build || ssb_window_fused on a "
-                               "forked stream, joined)",
+        "config": {"workload": WORKLOAD,
+                   "pipeline": ("ssb_sat_build_swa: ssb_sat_build || ssb_window_fused on a forked stream, joined"
+                                if world == 1 else
+                                "row bands: NCCL halo -> ssb_window_fused (side stream) || ssb_sat_prepare -> NCCL "
+                                "all-gather -> ssb_band_carry -> ssb_sat_finish (global table rows)"),
                    "parallelism": f"rowband{world}",
-                   "sat_path": "single-pass decoupled look-back" if os.environ.get("SSB_SAT_PATH", "").startswith("o")
-                   else "reduce-then-scan",
                    "l2": "inputs 5.95 GB >> 126 MB L2; no flush needed", "gen_s": round(gen_s, 1)},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": dom,
-                     "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms, "peak_source": pk["source"]},
-        "pipeline_roofline": {"bytes_per_step": b_alg, "achieved_gbs": b_alg / (ms_step * 1e-3) / 1e9,
-                              "frac": b_alg / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"],
-                              "bytes": "image read + table write + window sums write, each once"},
-        "phases_ms": phase_ms,
-        "phase_gbs": {k: b / (ms * 1e-3) / 1e9 for k, (b, ms) in kernels.items()},  # in context (overlapping)
+        "roofline": {"bound": "hbm", "achieved": achieved / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peak_all, "traffic": traffic,
+                     "traffic_over_algorithmic": (traffic / b_alg) if traffic else None,
+                     "kernel": "one step: ssb_sat_build (table) || ssb_window_fused (window sums), concurrent",
+                     "bytes_per_launch": b_alg, "ms_per_launch": ms_step,
+                     "bytes": "image read once + table written once + window sums written once (17 B/px); "
+                              "per GPU at N > 1",
+                     "peak_source": pk["source"]},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
 
-    # ---- the other pipelines on the same resident input (reported, not the headline)
-    def time_steps(fn):
-        for _ in range(3):
-            fn()
+    if world == 1 and not args.no_extra:
+        # per-kernel times in context: the same launches issued from here with
+        # events around each kernel group (untimed pass)
+        side = torch.cuda.Stream(dev)
+        ev = {"build": [], "windows": []}
+        for i in range(args.warmup + args.steps):
+            e0, e1, f0, f1 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            e0.record(stream)
+            side.wait_event(e0)
+            _lib.check(lib.ssb_sat_build(x_own.data_ptr(), kind.abi_code, ROWS, COLS, COLS, sat.data_ptr(), None,
+                                         ld, None, None, ws.data_ptr(), ws_bytes, None, sptr))
+            e1.record(stream)
+            f0.record(side)
+            _lib.check(lib.ssb_window_fused(x_own.data_ptr(), kind.abi_code, ROWS, COLS, COLS, W, _lib.SUM,
+                                            out.data_ptr(), None, None, OUT_C, None, 0, side.cuda_stream))
+            f1.record(side)
+            stream.wait_event(f1)
+            if i >= args.warmup:
+                ev["build"].append((e0, e1))
+                ev["windows"].append((f0, f1))
         barrier()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(args.steps):
-            fn()
-        a1.record(stream)
-        barrier()
-        return a0.elapsed_time(a1) / args.steps
+        result["phases_ms"] = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in ev.items()}
+        result["phases_ms"]["step"] = ms_step
 
-    try:
-        x = get_x()
+        def time_steps(fn):
+            for _ in range(3):
+                fn()
+            barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            a1.record(stream)
+            barrier()
+            return a0.elapsed_time(a1) / args.steps
 
         def sweep_step():
-            _lib.check(lib.ssb_sat_build(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), None, ld, None,
-                                         None, ws.data_ptr(), ws_bytes, None, sptr))
-            _lib.check(lib.ssb_window_eval(sat.data_ptr(), None, kind.abi_code, nr, COLS, ld, W, 1, _lib.SUM,
-                                           out.data_ptr(), None, None, out_c, sptr))
+            _lib.check(lib.ssb_sat_build(x_own.data_ptr(), kind.abi_code, ROWS, COLS, COLS, sat.data_ptr(), None, ld,
+                                         None, None, ws.data_ptr(), ws_bytes, None, sptr))
+            _lib.check(lib.ssb_window_eval(sat.data_ptr(), None, kind.abi_code, ROWS, COLS, ld, W, 1, _lib.SUM,
+                                           out.data_ptr(), None, None, OUT_C, sptr))
 
         def onepass_step():
-            _lib.check(lib.ssb_sat_build_swa_onepass(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), ld,
-                                                     W, _lib.SUM, out.data_ptr(), None, out_c, ws.data_ptr(),
-                                                     ws_bytes, sptr))
-
-        def swa_call_step():
-            _lib.check(lib.ssb_sat_build_swa(x.data_ptr(), kind.abi_code, nr, COLS, COLS, sat.data_ptr(), ld, W,
-                                             _lib.SUM, out.data_ptr(), None, out_c, ws.data_ptr(), ws_bytes, sptr))
-
-        for name, fn, b in (("corner_sweep_pipeline", sweep_step, b_mat), ("onepass_pipeline", onepass_step, b_alg),
-                            ("ssb_sat_build_swa_call", swa_call_step, b_alg)):
-            ms = time_steps(fn)
-            result[name] = {"value": rows * COLS / (ms * 1e-3) / 1e9, "ms_per_step": ms, "bytes_per_step": b,
-                            "roofline_frac": b / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
-        result["corner_sweep_pipeline"]["api"] = "ssb_sat_build -> ssb_window_eval (table read back)"
-        result["onepass_pipeline"]["api"] = "ssb_sat_build_swa_onepass"
-        result["ssb_sat_build_swa_call"]["api"] = "ssb_sat_build_swa (the headline step as one C-ABI call)"
-    except Exception as exc:  # pragma: no cover - reporting only
-        result["corner_sweep_pipeline"] = {"error": str(exc)}
-
-    # ---- fused window sums alone on the same resident input (no table)
-    try:
-        x = get_x()
+            _lib.check(lib.ssb_sat_build_swa_onepass(x_own.data_ptr(), kind.abi_code, ROWS, COLS, COLS,
+                                                     sat.data_ptr(), ld, W, _lib.SUM, out.data_ptr(), None, OUT_C,
+                                                     ws.data_ptr(), ws_bytes, sptr))
 
         def fused_step():
-            _lib.check(lib.ssb_window_fused(x.data_ptr(), kind.abi_code, nr, COLS, COLS, W, _lib.SUM,
-                                            out.data_ptr(), None, None, out_c, None, 0, sptr))
+            _lib.check(lib.ssb_window_fused(x_own.data_ptr(), kind.abi_code, ROWS, COLS, COLS, W, _lib.SUM,
+                                            out.data_ptr(), None, None, OUT_C, None, 0, sptr))
 
-        for _ in range(3):
-            fused_step()
-        barrier()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            fused_step()
-        f1.record(stream)
-        barrier()
-        fms = f0.elapsed_time(f1) / args.steps
-        fb = px_in + out_bytes
-        result["fused"] = {"value": rows * COLS / (fms * 1e-3) / 1e9, "ms_per_step": fms,
-                           "roofline_frac": fb / (fms * 1e-3) / 1e9 / pk["hbm_gbs"], "bytes_per_step": fb}
-    except Exception as exc:  # pragma: no cover - reporting only
-        result["fused"] = {"error": str(exc)}
+        for name, fn, b, api in (
+                ("corner_sweep_pipeline", sweep_step, b_mat, "ssb_sat_build -> ssb_window_eval (table read back)"),
+                ("onepass_pipeline", onepass_step, b_alg, "ssb_sat_build_swa_onepass"),
+                ("fused_windows_only", fused_step, px + out_bytes, "ssb_window_fused (no table)")):
+            try:
+                ms = time_steps(fn)
+                result[name] = {"value": px / (ms * 1e-3) / 1e9, "ms_per_step": ms, "bytes_per_step": b,
+                                "roofline_frac": b / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "api": api}
+            except Exception as exc:  # pragma: no cover - reporting only
+                result[name] = {"error": repr(exc)}
+        del sat, ws, out
+        torch.cuda.empty_cache()
 
     # ---- e2e through the public API with pinned host buffers: every rank runs
-    # swa on its own input rows (band + halo) and reads back its output band;
-    # the step time is the max over ranks
+    # swa on its own input rows (band + halo) on its own GPU and reads back its
+    # output band; the step time is the max over ranks
     if not args.no_e2e:
         try:
-            x_need = get_x()
-            del sat, ws
-            torch.cuda.empty_cache()
-            host_in = torch.empty((nr, COLS), dtype=torch.uint8, pin_memory=True)
-            _copy_chunks(host_in, x_need)
-            host_out = torch.empty((max(n_out, 1), out_c), dtype=torch.int64, pin_memory=True)
             import paper_2410_16291_b200 as sb
 
+            if world > 1:
+                del backend
+            torch.cuda.empty_cache()
+            x_need = shard.halo_exchange(x_own, ROWS, W, 1, storage=storage)
+            host_in = torch.empty((nr, COLS), dtype=torch.uint8, pin_memory=True)
+            for a in range(0, nr, 4096):
+                host_in[a:a + 4096].copy_(x_need[a:a + 4096].cpu())
+            host_out = torch.empty((max(n_out, 1), OUT_C), dtype=torch.int64, pin_memory=True)
             hin = host_in.numpy()
             hout = host_out.numpy().view(np.uint64)[:n_out]
 
             def e2e_step():
                 if n_out > 0:
-                    sb.swa(hin, W, "sum", pipeline="table", out=hout)
+                    sb.swa(hin, W, "sum", pipeline="table", out=hout, devices=[local])
 
             e2e_step()  # warm-up
             times = []
@@ -452,8 +565,8 @@ def main() -> None:
                 t0 = time.perf_counter()
                 e2e_step()
                 times.append(time.perf_counter() - t0)
-            te = sum(times) / len(times)
-            h2d, d2h = nr * COLS, n_out * out_c * 8
+            te = statistics.median(times)
+            h2d, d2h = nr * COLS, n_out * OUT_C * 8
             if world > 1:
                 import torch.distributed as dist
 
@@ -462,28 +575,26 @@ def main() -> None:
                 dist.all_reduce(mx, op=dist.ReduceOp.MAX)
                 dist.all_reduce(agg, op=dist.ReduceOp.SUM)
                 te, h2d, d2h = float(mx.item()), int(agg[1].item()), int(agg[2].item())
-            result["e2e"] = {"value": rows * COLS / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                             "d2h_bytes_per_step": d2h, "s_per_step": te,
-                             "api": "paper_2410_16291_b200.swa(numpy pinned, 256, 'sum', pipeline='table', out=pinned)"
-                                    " -> ssb_swa_host, per rank on its band + halo; max over ranks"}
+            result["e2e"] = {"value": px / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                             "d2h_bytes_per_step": d2h, "s_per_step": te, "steps_s": times,
+                             "d2h_gbs": d2h / te / 1e9,
+                             "api": "paper_2410_16291_b200.swa(pinned numpy, 256, 'sum', pipeline='table', out=pinned,"
+                                    " devices=[this GPU]) -> ssb_swa_host (banded H2D, table + windows, D2H); per "
+                                    "rank on its band + halo; median step, max over ranks"}
+            del host_in, host_out, hin, hout
         except Exception as exc:  # pragma: no cover
-            result["e2e"] = {"error": str(exc)}
+            result["e2e"] = {"error": repr(exc)}
 
-    # ---- CPU baseline: the reference algorithm on a bounded band, rank 0 at N=1
+    # ---- C1-C4 through the public API (N = 1)
+    if world == 1 and not args.no_configs:
+        result["configs"] = run_configs(args, dev, pk)
+
+    # ---- CPU baseline: the reference on a bounded band, rank 0 at N = 1
     if not args.no_cpu and world == 1 and rank == 0:
         try:
-            tot_t, tot_px = 0.0, 0
-            for _ in range(max(1, args.cpu_reps)):
-                dt, px = cpu_port_band(args.cpu_rows)
-                tot_t += dt
-                tot_px += px
-            result["cpu_baseline"] = {
-                "value": tot_px / tot_t / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                "sample": f"{args.cpu_reps} x C5 output rows [0, {args.cpu_rows}) ({args.cpu_rows + W - 1} input rows x "
-                          f"{COLS}); oracle.swa_threaded = numpy restatement of satsweep.swa_parallel; "
-                          f"{tot_t:.1f} s of CPU work"}
+            result["cpu_baseline"] = cpu_baseline(args)
         except Exception as exc:  # pragma: no cover
-            result["cpu_baseline"] = {"error": str(exc)}
+            result["cpu_baseline"] = {"error": repr(exc)}
 
     if rank == 0:
         emit(result)
@@ -491,11 +602,6 @@ def main() -> None:
         import torch.distributed as dist
 
         dist.destroy_process_group()
-
-
-def _copy_chunks(dst_host, src_dev, rows_per=4096):
-    for a in range(0, src_dev.shape[0], rows_per):
-        dst_host[a:a + rows_per].copy_(src_dev[a:a + rows_per].cpu())
 
 
 if __name__ == "__main__":

@@ -40,6 +40,19 @@ def pcie(nbytes=4 << 30, streams=1, reps=3):
 
 def main():
     bands = [int(a) for a in sys.argv[1:]] or [0]
+    # a C5-sized result read-back (47.3 GB) as one stream of 1.4 GB copies: the sustained ceiling
+    d = torch.empty(1400 << 20, dtype=torch.uint8, device="cuda")
+    big = torch.empty((34, 1400 << 20), dtype=torch.uint8, pin_memory=True)
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(34):
+            big[k].copy_(d, non_blocking=True)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    print(json.dumps({"sustained_d2h_47GB_s": ts, "gbs": [34 * (1400 << 20) / t / 1e9 for t in ts]}), flush=True)
+    del big, d
     print(json.dumps({"pcie_1stream": pcie(streams=1), "pcie_2streams": pcie(streams=2),
                       "sets": os.environ.get("SSB_HOST_SETS", "default")}), flush=True)
     img = synthetic.c5(threads=os.cpu_count())
