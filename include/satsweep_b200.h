@@ -239,6 +239,12 @@ int ssb_sharded_swa(int ndev, const int* devs, int in_dtype, int64_t rows, int64
 int ssb_band_carry(const void* parts, int band, int64_t len, int64_t parts_ld, int is_float, void* carry,
                    void* stream);
 
+/* Self-test: adds to *mismatches (device counter) the number of x[i] (device,
+ * n doubles) for which the finalisation's division by `divisor` (multiply by
+ * RN(1/divisor) + one FMA correction) differs in any bit from the IEEE
+ * division __ddiv_rn.  Asynchronous on `stream`. */
+int ssb_selftest_division(const double* x, int64_t n, double divisor, unsigned long long* mismatches, void* stream);
+
 /* Count of kernel launches the library issued since load (diagnostics). */
 int64_t ssb_launch_count(void);
 

@@ -13,9 +13,11 @@
 //            sat_segsum   per-(segment, strip) sum of those left carries,
 //            sat_topcarry exclusive scan down the segments of the segment
 //                         column totals (the table row above each segment).
-//   phase 3  sat_scan     per tile: warp row scans, transpose through
-//                         swizzled smem, column accumulation in registers,
-//                         128-bit coalesced streaming stores.
+//   phase 3  sat_scan     per warp tile: lane-serial row prefix + one warp
+//                         shuffle scan per row, the column accumulation in
+//                         the lane's registers (no smem transpose, no CTA
+//                         barrier), 256-bit streaming stores
+//                         (st.global.v4.b64; table rows 32-byte aligned).
 //
 // Both image-reading phases stage RB image rows per step into shared memory
 // with TMA bulk copies (cp.async.bulk, UBLKCP) on a 2-deep mbarrier pipeline,
@@ -608,10 +610,7 @@ bool onepass_supported(int dtype, bool sq);
 // DESIGN.md section 3); SSB_SAT_PATH=one routes ssb_sat_build through the
 // single-pass look-back kernel for A/B runs.
 static bool onepass_enabled(int dtype, bool sq) {
-  static const bool want_one = [] {
-    const char* e = getenv("SSB_SAT_PATH");
-    return e && e[0] == 'o';
-  }();
+  static const bool want_one = env_char("SSB_SAT_PATH") == 'o';
   return want_one && onepass_supported(dtype, sq);
 }
 

@@ -479,7 +479,7 @@ SweepPlan make_sweep_plan_t(int dtype, int64_t R, int64_t C, int64_t w) {
   sp.p = make_sat_plan(dtype, R, C, false);
   sp.nJw = (sp.p.nJ + SPW - 1) / SPW;
   const int64_t resident = (int64_t)kNumSMs * kSweepWarps * SSB_SWEEP_MINB;
-  const char* e = getenv("SSB_SWEEP_M");  // tuning: fixed segment multiple
+  static const int fixed_m = env_int("SSB_SWEEP_M", 0);  // tuning: fixed segment multiple
   int64_t best_m = 1;
   double best = 1e300;
   for (int64_t m = 1; m <= sp.p.nK; ++m) {
@@ -489,7 +489,7 @@ SweepPlan make_sweep_plan_t(int dtype, int64_t R, int64_t C, int64_t w) {
     const double cost = (double)((tiles + resident - 1) / resident) * (double)(min64(m * sp.p.SR, sp.p.PR) + w);
     if (cost < best) { best = cost; best_m = m; }
   }
-  if (e && atol(e) > 0) best_m = atol(e);
+  if (fixed_m > 0) best_m = fixed_m;
   sp.m = best_m;
   sp.SRs = best_m * sp.p.SR;
   sp.nKs = (int)((sp.p.PR + sp.SRs - 1) / sp.SRs);
@@ -540,6 +540,7 @@ cudaError_t launch_sweep_t(const void* in, int64_t R, int64_t C, int64_t in_ld, 
   FinalizeInt fi{};
   fi.n = (uint64_t)w * (uint64_t)w;
   fi.dn = (double)fi.n;
+  fi.inv_n = 1.0 / fi.dn;
   fi.u64_ok = true;
   fi.is_signed = std::is_same<InT, int32_t>::value;
   auto kfn = sat_sweep_kernel<InT, HW>;
@@ -570,10 +571,7 @@ cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_floa
 // 23.0 ms for the one-pass kernel above and 24.7 ms for build + corner sweep.
 // ssb_sat_build_swa_onepass (or SSB_SWA_PATH=onepass) runs the one-pass kernel.
 static bool swa_onepass_env() {
-  static const bool one = [] {
-    const char* e = getenv("SSB_SWA_PATH");
-    return e && e[0] == 'o';
-  }();
+  static const bool one = env_char("SSB_SWA_PATH") == 'o';
   return one;
 }
 

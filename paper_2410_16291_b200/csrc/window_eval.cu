@@ -39,9 +39,9 @@ template <> struct Fin<uint64_t> {
   __device__ __forceinline__ double std_(uint64_t s, uint64_t q) const { return fin_std_int(s, q, f); }
 };
 template <> struct Fin<double> {
-  double dn;
-  __device__ __forceinline__ double mean(double s) const { return fin_mean_f(s, dn); }
-  __device__ __forceinline__ double std_(double s, double q) const { return fin_std_f(s, q, dn); }
+  double dn, inv;
+  __device__ __forceinline__ double mean(double s) const { return fin_mean_f(s, dn, inv); }
+  __device__ __forceinline__ double std_(double s, double q) const { return fin_std_f(s, q, dn, inv); }
 };
 
 __device__ __forceinline__ void decode_item(const EvalGeom& g, int64_t it, int64_t& row, int64_t& cb) {
@@ -246,7 +246,7 @@ struct MultiEval {
   int64_t w[kMaxWin], out_r[kMaxWin], out_c[kMaxWin];
   WinOut o[kMaxWin];
   uint64_t n[kMaxWin];
-  double dn[kMaxWin];
+  double dn[kMaxWin], inv[kMaxWin];
   unsigned char u64_ok[kMaxWin];
   // stage layout (elements, per table): bottom segment at 0, top segment of
   // window k at off[k]; a stage is NT * stage_elems elements
@@ -258,12 +258,13 @@ template <typename Acc> struct FinK;
 template <> struct FinK<uint64_t> {
   __device__ static Fin<uint64_t> make(const MultiEval& m, int k) {
     Fin<uint64_t> f{};
-    f.f.n = m.n[k]; f.f.dn = m.dn[k]; f.f.u64_ok = m.u64_ok[k] != 0; f.f.is_signed = m.is_signed != 0;
+    f.f.n = m.n[k]; f.f.dn = m.dn[k]; f.f.inv_n = m.inv[k]; f.f.u64_ok = m.u64_ok[k] != 0;
+    f.f.is_signed = m.is_signed != 0;
     return f;
   }
 };
 template <> struct FinK<double> {
-  __device__ static Fin<double> make(const MultiEval& m, int k) { return Fin<double>{m.dn[k]}; }
+  __device__ static Fin<double> make(const MultiEval& m, int k) { return Fin<double>{m.dn[k], m.inv[k]}; }
 };
 
 // even number of elements covering [j0, j0 + CW + w) (reads reach index CW - 1 + w)
@@ -473,12 +474,11 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   used = false;
   constexpr int NT = SQ ? 2 : 1;
   constexpr int64_t kTmaCW = kThreads * U;
-  const char* env_b = getenv("SSB_EVAL_BATCH");
-  const int batch = env_b ? atoi(env_b) : 4;
-  const char* env_ns = getenv("SSB_EVAL_STAGES");
+  static const int batch = env_int("SSB_EVAL_BATCH", 4);
+  static const int env_ns = env_int("SSB_EVAL_STAGES", 0);
   // multi-window stages are large (a top segment per window): 2 stages keep
   // 3 CTAs per SM resident (C3 sweep 9.2 -> 8.5 ms); single window: 3 stages
-  int NS = env_ns ? atoi(env_ns) : (m.nwin > 1 ? 2 : 3);
+  int NS = env_ns > 0 ? env_ns : (m.nwin > 1 ? 2 : 3);
   if (NS < 2) NS = 2;
   if (NS > kTmaMaxNS) NS = kTmaMaxNS;
   // stage layout: bottom segment (covers the widest window), then one top
@@ -493,21 +493,21 @@ cudaError_t launch_tma_multi_u(const void* sat, const void* sat_sq, MultiEval m,
   if (smem > 220 * 1024 || (reinterpret_cast<uintptr_t>(sat) & 15) ||
       (SQ && (reinterpret_cast<uintptr_t>(sat_sq) & 15)) || (m.sat_ld & 1))
     return cudaSuccess;
-  const char* env_mb = getenv("SSB_EVAL_L2_MB");
+  static const double env_mb = env_double("SSB_EVAL_L2_MB", 0.0);
   int64_t out_c_max = 0;
   for (int k = 0; k < m.nwin; ++k) out_c_max = m.out_c[k] > out_c_max ? m.out_c[k] : out_c_max;
   // the panel's wmax + 1 most recent table rows stay hot in L2.  Single
   // window: 16 MB panels with evict_last on bottom rows / evict_first on top
   // rows (C5 sweep 15.14 -> 14.81 ms); the multi-window set measured best
   // without policies at 8 MB.
-  const double mb = env_mb ? atof(env_mb) : (m.nwin == 1 ? 16.0 : 8.0);
+  const double mb = env_mb > 0 ? env_mb : (m.nwin == 1 ? 16.0 : 8.0);
   m.pw = panel_width_max(out_c_max, m.wmax, SQ, kTmaCW, mb * 1024 * 1024);
   m.n_panels = (out_c_max + m.pw - 1) / m.pw;
   m.cpp = m.pw / kTmaCW;
   m.cpl = (out_c_max - (m.n_panels - 1) * m.pw + kTmaCW - 1) / kTmaCW;
   const bool multi = m.nwin > 1;
-  const char* env_h = getenv("SSB_EVAL_TMA_HINTS");  // tuning: L2 policies on the table row copies
-  const bool hints = env_h ? atoi(env_h) != 0 : !multi;
+  static const int env_h = env_int("SSB_EVAL_TMA_HINTS", -1);  // tuning: L2 policies on the table row copies
+  const bool hints = env_h >= 0 ? env_h != 0 : !multi;
   auto kfn = multi ? (hints ? window_eval_tma_kernel<Acc, SQ, U, true, true> : window_eval_tma_kernel<Acc, SQ, U, true, false>)
                    : (hints ? window_eval_tma_kernel<Acc, SQ, U, false, true> : window_eval_tma_kernel<Acc, SQ, U, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -535,8 +535,8 @@ template <typename Acc, bool SQ>
 cudaError_t launch_tma_multi(const void* sat, const void* sat_sq, const MultiEval& m, cudaStream_t st, bool& used) {
   // multi-window stages hold one top segment per window: narrower chunks keep
   // two CTAs per SM resident (tuning: SSB_EVAL_U=2|4)
-  const char* env_u = getenv("SSB_EVAL_U");
-  const int u = env_u ? atoi(env_u) : (m.nwin > 2 ? 2 : 4);
+  static const int env_u = env_int("SSB_EVAL_U", 0);
+  const int u = env_u > 0 ? env_u : (m.nwin > 2 ? 2 : 4);
   if (u == 1) return launch_tma_multi_u<Acc, SQ, 1>(sat, sat_sq, m, st, used);
   if (u == 2) return launch_tma_multi_u<Acc, SQ, 2>(sat, sat_sq, m, st, used);
   return launch_tma_multi_u<Acc, SQ, 4>(sat, sat_sq, m, st, used);
@@ -546,6 +546,7 @@ inline void fill_fin(MultiEval& m, int k, int in_dtype) {
   const uint64_t w = (uint64_t)m.w[k];
   m.n[k] = w * w;
   m.dn[k] = (double)(w * w);
+  m.inv[k] = 1.0 / m.dn[k];
   const uint64_t maxv = in_dtype == IN_U8 ? 255u : in_dtype == IN_U16 ? 65535u : 2147483648u;
   // stats.py:28-32: w^4 * max^2 <= 2^64 - 1  <=>  w^2 * max <= 2^32 - 1
   m.u64_ok[k] = ((unsigned __int128)(w * w) * maxv) <= (unsigned __int128)0xFFFFFFFFull ? 1 : 0;
@@ -589,14 +590,18 @@ inline EvalGeom make_eval_geom(int64_t R, int64_t C, int64_t w, int64_t s, int64
   return g;
 }
 
+inline int env_int_cached_hints() {
+  static const int h = env_int("SSB_EVAL_HINTS", 2);
+  return h;
+}
+
 template <typename Acc, bool SQ>
 cudaError_t launch_rows(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, cudaStream_t st) {
   constexpr int64_t CH = kRowChunk;
-  const char* env_mb = getenv("SSB_EVAL_L2_MB");
-  const char* env_k = getenv("SSB_EVAL_ROWS_IN_FLIGHT");
-  const char* env_h = getenv("SSB_EVAL_HINTS");
-  g.hints = env_h ? atoi(env_h) : 2;
-  g.pw = panel_width(g.out_c, g.w, 1, SQ, CH, (env_mb ? atof(env_mb) : 24.0) * 1024 * 1024);
+  static const double env_mb = env_double("SSB_EVAL_L2_MB", 24.0);
+  static const int env_k = env_int("SSB_EVAL_ROWS_IN_FLIGHT", 0);
+  g.hints = env_int_cached_hints();
+  g.pw = panel_width(g.out_c, g.w, 1, SQ, CH, env_mb * 1024 * 1024);
   g.n_panels = (g.out_c + g.pw - 1) / g.pw;
   g.cpp = g.pw / CH;
   g.cpl = (g.out_c - (g.n_panels - 1) * g.pw + CH - 1) / CH;
@@ -607,7 +612,7 @@ cudaError_t launch_rows(const void* sat, const void* sat_sq, EvalGeom g, WinOut 
                                                                  kThreads, 0);
   if (oe != cudaSuccess || per_sm < 1) per_sm = 1;
   int64_t k = (int64_t)kNumSMs * per_sm / g.cpp;
-  if (env_k && atoi(env_k) > 0 && atoi(env_k) < k) k = atoi(env_k);
+  if (env_k > 0 && env_k < k) k = env_k;
   if (k < 1) k = 1;
   if (k > g.out_r) k = g.out_r;
   const int blocks = (int)(k * g.cpp);
@@ -620,8 +625,8 @@ template <typename Acc>
 cudaError_t launch_eval_t(const void* sat, const void* sat_sq, EvalGeom g, WinOut o, Fin<Acc> fin, bool sq, int in_dtype,
                           cudaStream_t st) {
   if (g.s == 1) {
-    const char* env_path = getenv("SSB_EVAL_PATH");  // tuning: "ldg" forces the load-based sweep
-    if (!(env_path && env_path[0] == 'l')) {
+    static const bool ldg = env_char("SSB_EVAL_PATH") == 'l';  // tuning: "ldg" forces the load-based sweep
+    if (!ldg) {
       bool used = false;
       cudaError_t e = sq ? launch_tma<Acc, true>(sat, sat_sq, g, o, in_dtype, st, used)
                          : launch_tma<Acc, false>(sat, sat_sq, g, o, in_dtype, st, used);
@@ -645,12 +650,13 @@ cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_floa
   if (g.n_items <= 0) return cudaSuccess;
   cudaError_t e;
   if (is_float) {
-    Fin<double> fin{(double)(w * w)};
+    Fin<double> fin{(double)(w * w), 1.0 / (double)(w * w)};
     e = launch_eval_t<double>(sat, sat_sq, g, o, fin, sq, in_dtype, st);
   } else {
     Fin<uint64_t> fin{};
     fin.f.n = (uint64_t)(w * w);
     fin.f.dn = (double)(w * w);
+    fin.f.inv_n = 1.0 / fin.f.dn;
     const uint64_t maxv = in_dtype == IN_U8 ? 255u : in_dtype == IN_U16 ? 65535u : 2147483648u;
     // stats.py:28-32: w^4 * max^2 <= 2^64 - 1  <=>  w^2 * max <= 2^32 - 1
     fin.f.u64_ok = ((unsigned __int128)(uint64_t)(w * w) * maxv) <= (unsigned __int128)0xFFFFFFFFull;

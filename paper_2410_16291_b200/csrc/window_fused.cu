@@ -203,8 +203,8 @@ window_fused_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeI
           if constexpr (SQ) qv = sub(sm.pq[gg][j + w], sm.pq[gg][j]);
           if constexpr (kFloat) {
             if (g.mask & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + base + j, (double)sv);
-            if (g.mask & ST_MEAN) st_cs(o.mean + base + j, fin_mean_f((double)sv, fi.dn));
-            if (g.mask & ST_STD) st_cs(o.std_ + base + j, fin_std_f((double)sv, (double)qv, fi.dn));
+            if (g.mask & ST_MEAN) st_cs(o.mean + base + j, fin_mean_f((double)sv, fi.dn, fi.inv_n));
+            if (g.mask & ST_STD) st_cs(o.std_ + base + j, fin_std_f((double)sv, (double)qv, fi.dn, fi.inv_n));
           } else {
             // widen modular result: unsigned for u8/u16, sign-extended for i32
             uint64_t s64;
@@ -359,7 +359,7 @@ struct StripSmem {
   VQ pq[SQ ? NV + 64 : 1];
 };
 
-template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ, bool PACK>
+template <typename InT, int E, int RB, typename VT, typename VQ, bool SQ, bool PACK, int MASKT>
 __global__ void __launch_bounds__(32 * kStripWarps, SSB_FUSED_MINB)
 fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeInt fi, int nJ, int nK,
                    int* __restrict__ nonfinite) {
@@ -455,7 +455,8 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
 #pragma unroll
           for (int k = 0; k < E; ++k) {
             const InT xo = elem<InT>(oo, k);
-            if constexpr (kFloat) Vq[k] = sub(Vq[k], __dmul_rn((double)xo, (double)xo));
+            // x^2 of a float is exact in double, so the FMA rounds once, like mul + add
+            if constexpr (kFloat) Vq[k] = __fma_rn(-(double)xo, (double)xo, Vq[k]);
             else Vq[k] = sub(Vq[k], tv<VQ>(xo) * tv<VQ>(xo));
           }
         }
@@ -481,7 +482,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
 #pragma unroll
           for (int k = 0; k < E; ++k) {
             const InT xn = elem<InT>(on, k);
-            if constexpr (kFloat) Vq[k] = add(Vq[k], __dmul_rn((double)xn, (double)xn));
+            if constexpr (kFloat) Vq[k] = __fma_rn((double)xn, (double)xn, Vq[k]);
             else Vq[k] = add(Vq[k], tv<VQ>(xn) * tv<VQ>(xn));
           }
         }
@@ -543,6 +544,8 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
           else st_cs(dst, (uint64_t)sv);
         }
       } else {
+        // MASKT != 0: the stat set is a compile-time constant (no per-output tests)
+        const int mk = MASKT != 0 ? MASKT : g.mask;
         int a = addr_a, bw = addr_b;
         for (int qq = 0; qq < nq; ++qq, a += 33, bw += 33) {
           const int64_t at = obase + 32 * qq;
@@ -550,16 +553,16 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
           VQ qv = VQ(0);
           if constexpr (SQ) qv = sub(sm.pq[bw], sm.pq[a]);
           if constexpr (kFloat) {
-            if (g.mask & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + at, (double)sv);
-            if (g.mask & ST_MEAN) st_cs(o.mean + at, fin_mean_f((double)sv, fi.dn));
-            if (g.mask & ST_STD) st_cs(o.std_ + at, fin_std_f((double)sv, (double)qv, fi.dn));
+            if (mk & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + at, (double)sv);
+            if (mk & ST_MEAN) st_cs(o.mean + at, fin_mean_f((double)sv, fi.dn, fi.inv_n));
+            if (mk & ST_STD) st_cs(o.std_ + at, fin_std_f((double)sv, (double)qv, fi.dn, fi.inv_n));
           } else {
             uint64_t s64, q64 = 0;
             if constexpr (sizeof(VT) == 4) s64 = (uint64_t)(uint32_t)sv; else s64 = (uint64_t)sv;
             if constexpr (SQ) { if constexpr (sizeof(VQ) == 4) q64 = (uint64_t)(uint32_t)qv; else q64 = (uint64_t)qv; }
-            if (g.mask & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + at, s64);
-            if (g.mask & ST_MEAN) st_cs(o.mean + at, fin_mean_int(s64, fi));
-            if (g.mask & ST_STD) st_cs(o.std_ + at, fin_std_int(s64, q64, fi));
+            if (mk & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + at, s64);
+            if (mk & ST_MEAN) st_cs(o.mean + at, fin_mean_int(s64, fi));
+            if (mk & ST_STD) st_cs(o.std_ + at, fin_std_int(s64, q64, fi));
           }
         }
       }
@@ -570,7 +573,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
   if (nf && nonfinite) atomicOr(nonfinite, 1);
 }
 
-template <typename InT, int E, typename VT, typename VQ, bool SQ, bool PACK>
+template <typename InT, int E, typename VT, typename VQ, bool SQ, bool PACK, int MASKT = 0>
 cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK_override,
                            cudaStream_t st) {
   constexpr int ROWB = 32 * E * (int)sizeof(InT) + 48;
@@ -583,11 +586,11 @@ cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   if (nK < 1) nK = 1;
   g.sro = (g.out_r + nK - 1) / nK;
   nK = (g.out_r + g.sro - 1) / g.sro;
-  auto kfn = fused_strip_kernel<InT, E, RB, VT, VQ, SQ, PACK>;
+  auto kfn = fused_strip_kernel<InT, E, RB, VT, VQ, SQ, PACK, MASKT>;
   size_t smem = sizeof(SM) * kStripWarps;
   {  // tuning: SSB_FUSED_SMEM_KB pads the CTA's shared memory to cap CTAs per SM
      // (room for a concurrent kernel's CTAs on the same SMs)
-    static const long pad_kb = [] { const char* e = getenv("SSB_FUSED_SMEM_KB"); return e ? atol(e) : 0L; }();
+    static const long pad_kb = env_int("SSB_FUSED_SMEM_KB", 0);
     if ((size_t)pad_kb * 1024 > smem) smem = (size_t)pad_kb * 1024;
   }
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -599,6 +602,8 @@ cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   return cudaGetLastError();
 }
 
+template <typename T> constexpr bool kFloat_v = Elem<T>::kFloat;
+
 // uint8 with packed vertical sums (w <= 256, no squares): 64 bytes of raster
 // per lane and row (2048-column strips); otherwise 32 bytes per lane.  Falls
 // back to the CTA kernel below when fewer than 64 outputs per strip remain.
@@ -609,6 +614,20 @@ bool launch_strip(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* no
   if constexpr (sizeof(InT) == 1 && sizeof(VT) == 4 && !SQ) {
     if (g.w <= 256 && SSB_FUSED_PACK_E - 256 + 1 >= 64) {
       err = launch_strip_t<InT, SSB_FUSED_PACK_E / 32, VT, VQ, SQ, true>(in, g, o, fi, nonfinite, nK, st);
+      return true;
+    }
+  }
+  // 4-byte elements with wide windows: 512-column strips (16 per lane), so the
+  // w-1 halo columns cost less than with 256 (C2: w=100, C4: w=64)
+  if constexpr (sizeof(InT) == 4) {
+    if (g.w > 48 && 32 * 2 * E1 - g.w + 1 >= 64) {
+      // the BASELINE stat sets get a compile-time mask: C4 mean + std, C2 sum + mean
+      if (kFloat_v<InT> && SQ && g.mask == (ST_MEAN | ST_STD))
+        err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, false, ST_MEAN | ST_STD>(in, g, o, fi, nonfinite, nK, st);
+      else if (!SQ && g.mask == (ST_SUM | ST_MEAN))
+        err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, false, ST_SUM | ST_MEAN>(in, g, o, fi, nonfinite, nK, st);
+      else
+        err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, false>(in, g, o, fi, nonfinite, nK, st);
       return true;
     }
   }
@@ -627,8 +646,8 @@ constexpr int fused_group() {
 
 template <typename InT, typename VT, typename VQ, bool SQ>
 cudaError_t launch_fused_e(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK, cudaStream_t st) {
-  const char* env = getenv("SSB_FUSED_PATH");  // tuning: "cta" forces the CTA kernel
-  if (!(env && env[0] == 'c')) {
+  static const bool cta = env_char("SSB_FUSED_PATH") == 'c';  // tuning: "cta" forces the CTA kernel
+  if (!cta) {
     cudaError_t err = cudaSuccess;
     if (launch_strip<InT, VT, VQ, SQ>(in, g, o, fi, nonfinite, nK, st, err)) return err;
   }
@@ -654,6 +673,7 @@ cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C,
   FinalizeInt fi{};
   fi.n = (uint64_t)(w * w);
   fi.dn = (double)(w * w);
+  fi.inv_n = 1.0 / fi.dn;
   const double maxv = dtype == IN_U8 ? 255.0 : dtype == IN_U16 ? 65535.0 : 2147483648.0;
   fi.u64_ok = ((unsigned __int128)(uint64_t)(w * w) * (uint64_t)maxv) <= (unsigned __int128)0xFFFFFFFFull;
   fi.is_signed = dtype == IN_I32;

@@ -487,3 +487,30 @@ def test_lookback_build_large_matches_two_pass(sb, kind):
                                           ws.data_ptr(), wsb, st))
     torch.cuda.synchronize()
     assert torch.equal(a[:, : C + 1], b[:, : C + 1])
+
+
+def test_division_by_n_is_ieee(sb):
+    """The finalisation divides by n = w*w with a reciprocal multiply + FMA
+    correction; it must give the IEEE quotient bit for bit (stats.py:55-74 divide
+    with numpy's IEEE '/').  Integer window sums (every magnitude class, incl.
+    > 2^53), random doubles and f32 sums, for w = 1..300 and a few huge n."""
+    import torch
+
+    from paper_2410_16291_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(99)
+    ints = np.concatenate([np.arange(0, 200000, dtype=np.float64),
+                           rng.integers(0, 2**62, 200000).astype(np.float64),
+                           (rng.integers(0, 2**53, 200000)).astype(np.float64),
+                           -rng.integers(0, 2**40, 100000).astype(np.float64)])
+    floats = np.concatenate([rng.random(200000) * 10.0 ** rng.integers(-30, 30, 200000),
+                             rng.lognormal(0, 1, 200000) * 4096.0])
+    x = torch.from_numpy(np.concatenate([ints, floats])).to("cuda:0")
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda:0")
+    st = torch.cuda.current_stream().cuda_stream
+    ns = [w * w for w in range(1, 301)] + [10000, 4096, 65536 * 3 + 1, 3071 * 3071, 2**40 + 3]
+    for n in ns:
+        _lib.check(lib.ssb_selftest_division(x.data_ptr(), x.numel(), float(n), bad.data_ptr(), st))
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
