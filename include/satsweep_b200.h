@@ -245,6 +245,21 @@ int ssb_band_carry(const void* parts, int band, int64_t len, int64_t parts_ld, i
  * division __ddiv_rn.  Asynchronous on `stream`. */
 int ssb_selftest_division(const double* x, int64_t n, double divisor, unsigned long long* mismatches, void* stream);
 
+/* Write census (the device side of the reference's WriteCensus,
+ * parallel.py:35-51; tests/debug only).  While enabled on the calling thread,
+ * every table entry (r, c) a table build stores adds 1 to table_rows[r] and
+ * table_cols[c], and every output position a window kernel stores adds 1 to
+ * out_rows[i] (with several windows in one call, window k's rows follow those
+ * of windows 0..k-1).  Counters are caller-zeroed device uint64 arrays; NULL
+ * disables a kind (table_rows and table_cols go together).  Exactly-once
+ * coverage means table_rows[r] == cols+1, table_cols[c] == rows+1 and
+ * out_rows[i] == output cols.  One atomic per store: slow, never on by
+ * default.  ssb_swa_host (band-local rows) suspends it; ssb_sharded_swa
+ * refuses it. */
+int ssb_census_enable(unsigned long long* table_rows, int64_t n_table_rows, unsigned long long* table_cols,
+                      int64_t n_table_cols, unsigned long long* out_rows, int64_t n_out_rows);
+int ssb_census_disable(void);
+
 /* Count of kernel launches the library issued since load (diagnostics). */
 int64_t ssb_launch_count(void);
 

@@ -203,17 +203,31 @@ def choose_pipeline(pipeline: str, kind: ElemKind, w: int, stride: int) -> str:
     if pipeline == "table":
         return "table"
     # auto: integer results are exact on both pipelines, so take the cheaper
-    # one (measured, scripts/pipe_probe.py: the fused strip kernel wins for
-    # uint8 with w <= 256 and uint16 with w <= 128); float results keep the
-    # table pipeline so swa/multi_window/swa_integral agree bit for bit
-    # (integral.py:199-204).
+    # one (measured: the fused strip kernel wins for uint8 with w <= 256,
+    # uint16 with w <= 128 and int32 with w <= 256 -- C2 0.69 vs 0.74 ms).
+    # float results: see float_fused -- every entry point (swa, swa_integral,
+    # swa_parallel, multi_window) routes a float window the same way, so all
+    # methods still agree bit for bit (test_api.py:68-79).
     if not fusable:
         return "table"
     if kind is ElemKind.U8 and w <= 256:
         return "fused"
     if kind is ElemKind.U16 and w <= 128:
         return "fused"
+    if kind is ElemKind.I32 and w <= 256:
+        return "fused"
+    if float_fused(kind, w, stride):
+        return "fused"
     return "table"
+
+
+def float_fused(kind: ElemKind, w: int, stride: int) -> bool:
+    """Float windows evaluated without a table (vertical sliding sums + row
+    prefix in float64, window_fused.cu): stride 1 and w <= 256 (the 512-column
+    strips).  Measured at C4 (20,000 x 24,000 f32, mean + std, w=64) against the
+    table pipeline's 4.6 ms; the results differ from the table's only in
+    summation order (max rel. difference ~1e-10, rtol 1e-6 contract)."""
+    return kind is ElemKind.F32 and stride == 1 and w <= 256
 
 
 def run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None):

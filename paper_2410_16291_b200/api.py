@@ -95,12 +95,14 @@ def swa(array, window: int, stat: str = "sum", method: str = "parallel", stride:
     return _run(img, win, [kind], pipeline, outs, devices)[kind]
 
 
-def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str = "table") -> list:
-    """Several window sizes from one set of tables (api.py:58-67); stride 1.
+def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str = "auto") -> list:
+    """Several window sizes (api.py:58-67); stride 1.
 
-    The default ``pipeline="table"`` builds the table(s) once, like the
-    reference; ``"fused"``/``"auto"`` may evaluate integer rasters without a
-    table (bit-identical results)."""
+    ``"auto"``: integer rasters build the table once for the whole window set,
+    like the reference; float windows follow the same rule as ``swa`` (so
+    output i is bit-identical to ``swa(array, windows[i], stat)``).
+    ``"table"`` forces one table set for every window; ``"fused"`` evaluates
+    each window without a table."""
     img = _as_grid(array)
     specs = [WindowSpec(w) for w in windows]
     kind = StatKind.parse(stat)
@@ -108,9 +110,11 @@ def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str 
         raise ValueError("windows list must be non-empty")
     for s in specs:
         s.validate_for(img.rows, img.cols)
+    if pipeline not in ("auto", "table", "fused"):
+        raise ValueError(f"unknown pipeline {pipeline!r}; expected auto, table, or fused")
     from .integral import _run_tables
 
-    if pipeline == "table" or _engine.choose_pipeline(pipeline, img.elem_kind, max(windows), 1) == "table":
+    if pipeline in ("auto", "table"):
         grid = img if img.on_device else ImageGrid(img.values, img.elem_kind, _check_finite=False)
-        return [r.values for r in _run_tables(grid, specs, kind)]
+        return [r.values for r in _run_tables(grid, specs, kind, force_table=pipeline == "table")]
     return [swa(array, s.w, kind.value, pipeline="fused") for s in specs]

@@ -143,6 +143,13 @@ struct DeviceGuard {
   if (device_guard_.err != cudaSuccess) return cuda_fail(device_guard_.err, "stream device")
 }  // namespace
 
+// the calling thread's write census (ssb_census_enable); kernels launched by
+// this thread while it is set count their stores into it
+namespace {
+thread_local Census t_census;
+}
+Census ssb::census_sink() { return t_census; }
+
 // shard.cu and io.cu report through the same thread-local message
 int ssb::shard_fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -169,6 +176,21 @@ int ssb::io_fail(int code, const char* fmt, ...) {
 extern "C" {
 
 int ssb_abi_version(void) { return SSB_ABI_VERSION; }
+
+int ssb_census_enable(unsigned long long* table_rows, int64_t n_table_rows, unsigned long long* table_cols,
+                      int64_t n_table_cols, unsigned long long* out_rows, int64_t n_out_rows) {
+  if ((table_rows && n_table_rows < 1) || (table_cols && n_table_cols < 1) || (out_rows && n_out_rows < 1) ||
+      (!table_rows != !table_cols))
+    return fail(SSB_EINVAL, "bad census buffers");
+  t_census = Census{table_rows, table_cols, out_rows, table_rows ? n_table_rows : 0, table_cols ? n_table_cols : 0,
+                    out_rows ? n_out_rows : 0};
+  return SSB_OK;
+}
+
+int ssb_census_disable(void) {
+  t_census = Census{};
+  return SSB_OK;
+}
 const char* ssb_last_error(void) { return t_err.c_str(); }
 int64_t ssb_launch_count(void) { return (int64_t)g_launches.load(); }
 int64_t ssb_window_fused_max_w(void) { return kFusedMaxWindow; }
@@ -480,6 +502,13 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   if (out_ld < out_c) return fail(SSB_EINVAL, "out_ld < output cols");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  // the bands' kernels see band-local rows: the write census covers the
+  // device entry points only, so it is suspended for this call
+  struct CensusPause {
+    Census saved = t_census;
+    CensusPause() { t_census = Census{}; }
+    ~CensusPause() { t_census = saved; }
+  } census_pause;
 
   // band geometry: output rows [o0, o1) need input rows [o0*s, (o1-1)*s + w)
   const int64_t sat_ld = ((cols + 1) + 3) & ~int64_t(3);  // 32-byte aligned rows

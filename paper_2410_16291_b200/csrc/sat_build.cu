@@ -377,7 +377,7 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
                 typename Elem<InT>::Acc* __restrict__ sat, typename Elem<InT>::Acc* __restrict__ sat_sq, int64_t sat_ld,
                 const typename Elem<InT>::Acc* __restrict__ rl, const typename Elem<InT>::Acc* __restrict__ rl_sq,
                 const typename Elem<InT>::Acc* __restrict__ top, const typename Elem<InT>::Acc* __restrict__ top_sq,
-                int64_t SR, int nJ, int nK) {
+                int64_t SR, int nJ, int nK, Census cz) {
   using Tr = Elem<InT>;
   using Loc = typename Tr::Loc;
   using LocSq = typename Tr::LocSq;
@@ -469,6 +469,15 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
         }
         store_lane_cols<Acc, E>(sat_sq + row * sat_ld + cbase, accq, cbase, PC);
       }
+      if (cz.trow != nullptr) {  // census: table positions (row, col) this lane stored
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (cbase + k < PC) {
+            census_add(cz.trow, cz.ntr, row);
+            census_add(cz.tcol, cz.ntc, cbase + k);
+          }
+        }
+      }
     }
     __syncwarp();  // stage s fully read before it is refilled
   }
@@ -559,7 +568,8 @@ cudaError_t launch_sat_finish_t(const void* in, int64_t R, int64_t C, int64_t in
   if (e != cudaSuccess) return e;
   sat_scan_kernel<InT, SQ><<<tb, 32 * kScanWarps, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
                                                     reinterpret_cast<Acc*>(sat), reinterpret_cast<Acc*>(sat_sq),
-                                                    sat_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ, p.nK);
+                                                    sat_ld, rowtot, rowtot_sq, colp, colp_sq, p.SR, p.nJ, p.nK,
+                                                    census_sink());
   note_launch(1);
   return cudaGetLastError();
 }

@@ -237,6 +237,8 @@ int ssb_sharded_swa(int ndev, const int* devs, int in_dtype, int64_t rows, int64
   int prev = 0;
   cudaError_t e = cudaGetDevice(&prev);
   if (e != cudaSuccess) return shard_cuda_fail(e, "cudaGetDevice");
+  if (census_sink().trow || census_sink().orow)  // bands write band-local rows
+    return shard_fail(SSB_EUNSUPPORTED, "the write census covers single-device entry points only");
   std::vector<cudaEvent_t> ev_in(ndev, nullptr), ev_tot(ndev, nullptr), ev_done(ndev, nullptr);
   int status = SSB_OK;
   auto cf = [&](cudaError_t ce, const char* where) {

@@ -28,6 +28,7 @@ struct EvalGeom {
   int mask;
   int vec_out;  // output rows aligned for VW-wide stores
   int hints;    // L2 policy: 0 none, 1 bottom evict_last + top evict_first, 2 top evict_first only
+  Census cz;
 };
 
 constexpr int kChunk = 2 * kThreads;  // 512 output columns per work item
@@ -100,6 +101,7 @@ window_eval_gen_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
       Acc q0 = Acc(0);
       if constexpr (SQ) q0 = corner4(__ldg(sq + bot + r), __ldg(sq + top + r), __ldg(sq + bot + l), __ldg(sq + top + l));
       emit_pair<Acc>(g, o, fin, i, j, s0, s0, q0, q0, false, false);
+      census_add(g.cz.orow, g.cz.nor, i);
     }
   }
 }
@@ -195,6 +197,7 @@ window_eval_rows_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq,
         if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, s[u]);
         if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(s[u]));
         if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(s[u], qq[u]));
+        census_add(g.cz.orow, g.cz.nor, i);
       }
     }
   }
@@ -252,6 +255,8 @@ struct MultiEval {
   // window k at off[k]; a stage is NT * stage_elems elements
   int off[kMaxWin];
   int stage_elems;
+  Census cz;
+  int64_t census_off[kMaxWin];  // first census row of window k
 };
 
 template <typename Acc> struct FinK;
@@ -440,6 +445,7 @@ window_eval_tma_kernel(const Acc* __restrict__ sat, const Acc* __restrict__ sq, 
           if (g.mask & ST_SUM) st_cs(reinterpret_cast<Acc*>(o.sum) + at, sv[u]);
           if (g.mask & ST_MEAN) st_cs(o.mean + at, fin.mean(sv[u]));
           if constexpr (SQ) if (g.mask & ST_STD) st_cs(o.std_ + at, fin.std_(sv[u], qv[u]));
+          census_add(g.cz.orow, g.cz.nor, g.census_off[k] + (rb - w));
         }
       };
       if constexpr (MULTI) {
@@ -564,6 +570,8 @@ cudaError_t launch_tma(const void* sat, const void* sat_sq, EvalGeom g, WinOut o
   m.R = g.out_r + g.w - 1;
   m.sat_ld = g.sat_ld;
   m.w[0] = g.w; m.out_r[0] = g.out_r; m.out_c[0] = g.out_c; m.o[0] = o;
+  m.cz = g.cz;
+  m.census_off[0] = 0;
   fill_fin(m, 0, in_dtype);
   return launch_tma_multi<Acc, SQ>(sat, sat_sq, m, st, used);
 }
@@ -573,6 +581,7 @@ inline EvalGeom make_eval_geom(int64_t R, int64_t C, int64_t w, int64_t s, int64
   g.out_r = (R - w) / s + 1;
   g.out_c = (C - w) / s + 1;
   g.w = w; g.s = s; g.sat_ld = sat_ld; g.mask = mask;
+  g.cz = census_sink();
   // panel: keep (w*s + 1) table rows of the panel (both tables) in ~48 MB of L2
   const double budget = 48.0 * 1024 * 1024;
   const double row_bytes = 8.0 * (sq ? 2 : 1) * (double)(w + 1);
@@ -676,6 +685,7 @@ cudaError_t launch_window_eval_multi(const void* sat, const void* sat_sq, bool i
   MultiEval m{};
   m.nwin = nwin;
   m.mask = mask;
+  m.cz = census_sink();
   m.is_signed = in_dtype == IN_I32;
   m.R = R;
   m.sat_ld = sat_ld;
@@ -686,6 +696,7 @@ cudaError_t launch_window_eval_multi(const void* sat, const void* sat_sq, bool i
     m.out_r[k] = R - ws[k] + 1;
     m.out_c[k] = C - ws[k] + 1;
     m.o[k] = outs[k];
+    m.census_off[k] = k == 0 ? 0 : m.census_off[k - 1] + m.out_r[k - 1];
     m.wmin = ws[k] < m.wmin ? ws[k] : m.wmin;
     m.wmax = ws[k] > m.wmax ? ws[k] : m.wmax;
     fill_fin(m, k, in_dtype);

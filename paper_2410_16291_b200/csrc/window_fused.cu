@@ -76,6 +76,7 @@ struct FusedGeom {
   int64_t sro;  // output rows per segment
   int mask;
   int vec_ok;
+  Census cz;
 };
 
 template <typename InT, typename VT, typename VQ, bool SQ, int E, int G>
@@ -219,6 +220,7 @@ window_fused_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeI
             if (g.mask & ST_MEAN) st_cs(o.mean + base + j, fin_mean_int(s64, fi));
             if (g.mask & ST_STD) st_cs(o.std_ + base + j, fin_std_int(s64, q64, fi));
           }
+          census_add(g.cz.orow, g.cz.nor, i);
         }
       }
     }
@@ -280,7 +282,8 @@ __device__ __forceinline__ void st_pair(uint64_t* p, uint64_t a, uint64_t b) {
 
 template <int E>
 __device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint32_t* P, int64_t gb,
-                                                uint64_t* __restrict__ out, int nout, int w, int lane) {
+                                                uint64_t* __restrict__ out, int nout, int w, int lane,
+                                                const Census& cz, int64_t i) {
   const int d = (int)((reinterpret_cast<uintptr_t>(out + gb) >> 3) & 1);  // 16-byte phase of output 0
   uint32_t tot = 0u;
 #pragma unroll
@@ -303,8 +306,11 @@ __device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint
   __syncwarp();
   uint64_t* orow = out + gb;
   if (lane == 0) {
-    if (d) orow[0] = (uint64_t)(P[pp(w + 1)] - P[pp(1)]);                         // leading single
-    if ((nout - d) & 1) orow[nout - 1] = (uint64_t)(P[pp(nout - 1 + w + d)] - P[pp(nout - 1 + d)]);  // trailing
+    if (d) { orow[0] = (uint64_t)(P[pp(w + 1)] - P[pp(1)]); census_add(cz.orow, cz.nor, i); }  // leading single
+    if ((nout - d) & 1) {                                                                       // trailing
+      orow[nout - 1] = (uint64_t)(P[pp(nout - 1 + w + d)] - P[pp(nout - 1 + d)]);
+      census_add(cz.orow, cz.nor, i);
+    }
   }
   const int npair = (nout - d) >> 1;
   // pair m: outputs j = d + 2m, d + 2m + 1; P words at pp(j + d) (even) and pp(j + w + d)
@@ -319,6 +325,7 @@ __device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint
       const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
       const uint2 B = *reinterpret_cast<const uint2*>(pb + 66 * qq);
       st_pair(dst + 64 * qq, (uint64_t)(B.x - A.x), (uint64_t)(B.y - A.y));
+      census_add(cz.orow, cz.nor, i, 2ull);
     }
   } else {
     const uint32_t* pb0 = P + pp(vb);
@@ -327,6 +334,7 @@ __device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint
     for (int qq = 0; qq < nq; ++qq) {
       const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
       st_pair(dst + 64 * qq, (uint64_t)(pb0[66 * qq] - A.x), (uint64_t)(pb1[66 * qq] - A.y));
+      census_add(cz.orow, cz.nor, i, 2ull);
     }
   }
   __syncwarp();  // P is rewritten by the next row
@@ -491,7 +499,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
       const int64_t i = r - (w - 1);
       if constexpr (PACK) {
         if (g.mask == ST_SUM) {  // uint8 sums: packed prefix + paired outputs
-          packed_sums_row<E>(V, sm.p, i * o.ld + oc0, reinterpret_cast<uint64_t*>(o.sum), nout, w, lane);
+          packed_sums_row<E>(V, sm.p, i * o.ld + oc0, reinterpret_cast<uint64_t*>(o.sum), nout, w, lane, g.cz, i);
           continue;
         }
       }
@@ -505,10 +513,9 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
             return V[k];
           }
         };
-        VT tot = VT(0);
-#pragma unroll
-        for (int k = 0; k < E; ++k) tot = add(tot, vcol(k));
-        VT run = sub(warp_incl_scan(tot, lane), tot);
+        // lane total by a pairwise tree (one short dependency chain), the
+        // lanes to the left by an exclusive warp scan, then the running prefix
+        VT run = warp_excl_scan(tree_sum<E, VT>(vcol), lane);
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           run = add(run, vcol(k));
@@ -518,10 +525,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
         if (lane == 0) sm.p[0] = VT(0);
       }
       if constexpr (SQ) {
-        VQ tot = VQ(0);
-#pragma unroll
-        for (int k = 0; k < E; ++k) tot = add(tot, Vq[k]);
-        VQ run = sub(warp_incl_scan(tot, lane), tot);
+        VQ run = warp_excl_scan(tree_sum<E, VQ>([&](int k) { return Vq[k]; }), lane);
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           run = add(run, Vq[k]);
@@ -542,28 +546,34 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
           const VT sv = sub(sm.p[bw], sm.p[a]);
           if constexpr (sizeof(VT) == 4) st_cs(dst, (uint64_t)(uint32_t)sv);
           else st_cs(dst, (uint64_t)sv);
+          census_add(g.cz.orow, g.cz.nor, i);
         }
       } else {
         // MASKT != 0: the stat set is a compile-time constant (no per-output tests)
         const int mk = MASKT != 0 ? MASKT : g.mask;
         int a = addr_a, bw = addr_b;
-        for (int qq = 0; qq < nq; ++qq, a += 33, bw += 33) {
-          const int64_t at = obase + 32 * qq;
+        // output pointers advance by 32 per step (no 64-bit index arithmetic
+        // per output); a stat that is not requested is never dereferenced
+        uint64_t* p_sum = reinterpret_cast<uint64_t*>(o.sum) + obase;
+        double* p_mean = o.mean + obase;
+        double* p_std = o.std_ + obase;
+        for (int qq = 0; qq < nq; ++qq, a += 33, bw += 33, p_sum += 32, p_mean += 32, p_std += 32) {
           const VT sv = sub(sm.p[bw], sm.p[a]);
           VQ qv = VQ(0);
           if constexpr (SQ) qv = sub(sm.pq[bw], sm.pq[a]);
           if constexpr (kFloat) {
-            if (mk & ST_SUM) st_cs(reinterpret_cast<double*>(o.sum) + at, (double)sv);
-            if (mk & ST_MEAN) st_cs(o.mean + at, fin_mean_f((double)sv, fi.dn, fi.inv_n));
-            if (mk & ST_STD) st_cs(o.std_ + at, fin_std_f((double)sv, (double)qv, fi.dn, fi.inv_n));
+            if (mk & ST_SUM) st_cs(reinterpret_cast<double*>(p_sum), (double)sv);
+            if (mk & ST_MEAN) st_cs(p_mean, fin_mean_f((double)sv, fi.dn, fi.inv_n));
+            if (mk & ST_STD) st_cs(p_std, fin_std_f((double)sv, (double)qv, fi.dn, fi.inv_n));
           } else {
             uint64_t s64, q64 = 0;
             if constexpr (sizeof(VT) == 4) s64 = (uint64_t)(uint32_t)sv; else s64 = (uint64_t)sv;
             if constexpr (SQ) { if constexpr (sizeof(VQ) == 4) q64 = (uint64_t)(uint32_t)qv; else q64 = (uint64_t)qv; }
-            if (mk & ST_SUM) st_cs(reinterpret_cast<uint64_t*>(o.sum) + at, s64);
-            if (mk & ST_MEAN) st_cs(o.mean + at, fin_mean_int(s64, fi));
-            if (mk & ST_STD) st_cs(o.std_ + at, fin_std_int(s64, q64, fi));
+            if (mk & ST_SUM) st_cs(p_sum, s64);
+            if (mk & ST_MEAN) st_cs(p_mean, fin_mean_int(s64, fi));
+            if (mk & ST_STD) st_cs(p_std, fin_std_int(s64, q64, fi));
           }
+          census_add(g.cz.orow, g.cz.nor, i);
         }
       }
       __syncwarp();
@@ -664,6 +674,7 @@ cudaError_t launch_window_fused(const void* in, int dtype, int64_t R, int64_t C,
   if (w < 1 || w > kFusedMaxW) return cudaErrorInvalidValue;
   FusedGeom g{};
   g.R = R; g.C = C; g.in_ld = in_ld; g.w = (int)w; g.mask = mask;
+  g.cz = census_sink();
   g.out_r = R - w + 1; g.out_c = C - w + 1;
   const int es = dtype == IN_U8 ? 1 : dtype == IN_U16 ? 2 : 4;
   const int E = w <= 256 ? 4 : w <= 1024 ? 8 : 16;

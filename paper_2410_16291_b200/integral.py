@@ -187,7 +187,7 @@ def _finish(img: ImageGrid, stats, res) -> dict:
 
 
 @_engine.device_scoped
-def _run_tables(img: ImageGrid, wins, stat: StatKind):
+def _run_tables(img: ImageGrid, wins, stat: StatKind, force_table: bool = False):
     """Tables once, then the corner sweep(s) (integral.py:166-189, :199-210).
 
     Stride-1 window sets go through ssb_window_eval_multi: one pass over the
@@ -197,6 +197,23 @@ def _run_tables(img: ImageGrid, wins, stat: StatKind):
     x, dev = _engine.device_input(img)
     flag = _engine.new_flag(dev) if img.elem_kind is ElemKind.F32 else None
     sq_needed = needs_squares(stat)
+    if not force_table and img.elem_kind is ElemKind.F32:
+        # float windows eligible for the fused kernel take it on every entry
+        # point (_engine.float_fused), one launch per window; the others share
+        # one table set
+        fz = [_engine.float_fused(img.elem_kind, w.w, w.stride) for w in wins]
+        if any(fz):
+            rest = iter(_run_tables(img, [w for w, f in zip(wins, fz) if not f], stat, force_table=True)
+                        if not all(fz) else [])
+            out = []
+            for win, f in zip(wins, fz):
+                if f:
+                    r = _engine.fused(x, img.elem_kind, img.rows, img.cols, win.w, (stat,), dev, flag=flag)
+                    _engine.check_nonfinite(flag)
+                    out.append(ResultGrid(stat, _finish(img, (stat,), r)[stat]))
+                else:
+                    out.append(next(rest))
+            return out
     if len(wins) == 1 and _engine.sweep_supported(img.elem_kind, wins[0].w, wins[0].stride, (stat,)):
         # one window: table and sweep in one pass (the table stays in scratch)
         _, _, outs = _engine.table_and_sweep(x, img.elem_kind, img.rows, img.cols, wins[0].w, (stat,), dev,

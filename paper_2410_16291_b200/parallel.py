@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .grid import ImageGrid, ResultGrid, StatKind, WindowSpec
+from .grid import ImageGrid, ResultGrid, StatKind, WindowSpec, output_dims
 from .integral import IntegralImage, _build, _run_tables, select_accum  # noqa: F401
 from .stats import needs_squares
 
@@ -86,38 +86,98 @@ def sat_tiling(img: ImageGrid, squared: bool) -> tuple[int, int, int, int]:
     return tuple(int(v) for v in info)
 
 
-def _census_build(census: WriteCensus | None, img: ImageGrid, squared: bool, suffix: str) -> None:
-    if census is None:
-        return
-    tw, sr, n_j, n_k = sat_tiling(img, squared)
-    pr, pc = img.rows + 1, img.cols + 1
-    for k in range(n_k):  # table rows [k0, k1) hold image rows [k0-1, k1-1)
-        lo, hi = max(k * sr - 1, 0), min((k + 1) * sr, pr) - 1
-        if hi > lo:
-            census.record(f"rows/{suffix}", lo, hi)
-    for j in range(n_j):
-        lo, hi = max(j * tw - 1, 0), min((j + 1) * tw, pc) - 1
-        if hi > lo:
-            census.record(f"cols/{suffix}", lo, hi)
+class _DeviceCensus:
+    """Counters the kernels themselves write while the census is enabled
+    (ssb_census_enable): one per table row, table column and output row.  On
+    exit the counts become WriteCensus records, so ``assert_disjoint_cover``
+    checks what the device actually stored: index i is recorded once when its
+    count is exactly one full row/column of stores, twice when it was stored
+    more often or only partly (an overlap or a partial write fails the check),
+    and not at all when nothing was stored (a gap fails it)."""
+
+    def __init__(self, census: WriteCensus, img: ImageGrid, out_dims=None, table: bool = True):
+        self.census, self.img, self.out_dims, self.table = census, img, out_dims, table
+
+    def __enter__(self):
+        import torch
+
+        from . import _device
+
+        dev = _device.current_device()
+        pr, pc = self.img.rows + 1, self.img.cols + 1
+        z = lambda n: torch.zeros(max(n, 1), dtype=torch.int64, device=dev)  # noqa: E731
+        self.trow, self.tcol = (z(pr), z(pc)) if self.table else (None, None)
+        self.orow = z(self.out_dims[0]) if self.out_dims else None
+        p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        _lib.check(_lib.load().ssb_census_enable(p(self.trow), pr, p(self.tcol), pc, p(self.orow),
+                                                 self.out_dims[0] if self.out_dims else 0), "census")
+        return self
+
+    def __exit__(self, *exc):
+        import torch
+
+        _lib.load().ssb_census_disable()
+        if exc[0] is not None:
+            return False
+        torch.cuda.synchronize()
+        self.counts = {k: None if t is None else t.cpu().numpy() for k, t in
+                       (("trow", self.trow), ("tcol", self.tcol), ("orow", self.orow))}
+        return False
+
+    def record(self, phase: str, which: str, expected: int, skip: int = 0) -> None:
+        """counts[skip:] -> census records for indices 0.. (skip = the table's zero border)."""
+        c = self.counts[which][skip:]
+        full = c == expected
+        i, n = 0, c.size
+        while i < n:
+            if full[i]:  # one record per run of exactly-covered indices
+                j = i
+                while j < n and full[j]:
+                    j += 1
+                self.census.record(phase, i, j)
+                i = j
+                continue
+            if c[i] != 0:  # over- or partially-written: a double record fails the check
+                self.census.record(phase, i, i + 1)
+                self.census.record(phase, i, i + 1)
+            i += 1
+
+    def record_table(self, suffixes) -> None:
+        pr, pc = self.img.rows + 1, self.img.cols + 1
+        for sfx in suffixes:
+            self.record(f"rows/{sfx}", "trow", pc, skip=1)
+            self.record(f"cols/{sfx}", "tcol", pr, skip=1)
+        # the zero border row/column are stores too: exactly one full row / column
+        if self.counts["trow"][0] != pc or self.counts["tcol"][0] != pr:
+            for sfx in suffixes:
+                self.census.record(f"rows/{sfx}", 0, 1)  # forces a failed check on the border
 
 
 def build_sat_parallel(img: ImageGrid, squared: bool = False, cfg: ParallelConfig | None = None) -> IntegralImage:
     """Same table as build_sat, for every worker count (parallel.py:106-121)."""
     cfg = cfg or ParallelConfig()
-    _census_build(cfg.census, img, squared, "sq" if squared else "sum")
-    return _build(img, squared)
+    if cfg.census is None:
+        return _build(img, squared)
+    with _DeviceCensus(cfg.census, img) as dc:
+        table = _build(img, squared)
+    dc.record_table(["sq" if squared else "sum"])
+    return table
 
 
 def swa_parallel(img: ImageGrid, win: WindowSpec, stat: StatKind, cfg: ParallelConfig | None = None) -> ResultGrid:
     """Table build plus corner sweep; bit-identical to swa_integral (parallel.py:137-149)."""
     cfg = cfg or ParallelConfig()
     win.validate_for(img.rows, img.cols)
-    if cfg.census is not None:
-        _census_build(cfg.census, img, needs_squares(stat), "sum")
-        if needs_squares(stat):
-            _census_build(cfg.census, img, True, "sq")
-        out_r = (img.rows - win.w) // win.stride + 1
-        cfg.census.record("query/sum", 0, out_r)
-        if needs_squares(stat):
-            cfg.census.record("query/sq", 0, out_r)
-    return _run_tables(img, [win], stat)[0]
+    if cfg.census is None:
+        return _run_tables(img, [win], stat)[0]
+    out_r, out_c = output_dims(img.rows, img.cols, win)
+    # the kernels count their own stores: table entries (the plain and squared
+    # tables are written by one kernel) and output positions
+    with _DeviceCensus(cfg.census, img, (out_r, out_c)) as dc:
+        res = _run_tables(img, [win], stat)[0]
+    sq = needs_squares(stat)
+    dc.record_table(["sum", "sq"] if sq else ["sum"])
+    dc.record("query/sum", "orow", out_c)
+    if sq:
+        dc.record("query/sq", "orow", out_c)
+    return res

@@ -259,6 +259,73 @@ def test_parallel_census_and_identity(sb, rng):
         census.assert_disjoint_cover(phase, total)
 
 
+@pytest.mark.parametrize("kind,w,s,stat,shape", [("u8", 9, 1, "sum", (300, 517)), ("u8", 17, 1, "mean", (300, 517)),
+                                                ("f32", 6, 1, "std", (300, 517)), ("u16", 5, 3, "sum", (300, 517)),
+                                                ("i32", 4, 1, "mean", (300, 517)),
+                                                ("u8", 64, 1, "sum", (4100, 4100))])  # >= 2^24 px: fused windows
+def test_device_census_exactly_once(sb, rng, kind, w, s, stat, shape):
+    """The census is written by the kernels (one atomic per stored table entry /
+    output position): every table row, column and output row is covered exactly
+    once on every pipeline the parallel entry points take (parallel.py:35-51,
+    pkg/tests/test_parallel.py:90-118)."""
+    R, C = shape
+    if kind == "i32":
+        v = rng.integers(-1000, 1000, size=(R, C)).astype(np.int32)
+    else:
+        v = random_values(rng, R, C, kind)
+    census = sb.WriteCensus()
+    cfg = sb.ParallelConfig(census=census)
+    win = sb.WindowSpec(w, s)
+    sb.swa_parallel(sb.ImageGrid(v), win, sb.StatKind(stat), cfg)
+    out_r, _ = sb.output_dims(R, C, win)
+    phases = [("rows/sum", R), ("cols/sum", C), ("query/sum", out_r)]
+    if stat == "std":
+        phases += [("rows/sq", R), ("cols/sq", C), ("query/sq", out_r)]
+    for phase, total in phases:
+        census.assert_disjoint_cover(phase, total)
+    c2 = sb.WriteCensus()
+    sb.build_sat_parallel(sb.ImageGrid(v), False, sb.ParallelConfig(census=c2))
+    c2.assert_disjoint_cover("rows/sum", R)
+    c2.assert_disjoint_cover("cols/sum", C)
+
+
+def test_device_census_sees_double_writes(sb, rng):
+    """Two builds inside one census window store every entry twice: the check must fail."""
+    import torch
+
+    from paper_2410_16291_b200.parallel import _DeviceCensus
+
+    v = random_values(rng, 64, 80, "u8")
+    img = sb.ImageGrid(v)
+    census = sb.WriteCensus()
+    with _DeviceCensus(census, img) as dc:
+        sb.build_sat(img)
+        sb.build_sat(img)
+    torch.cuda.synchronize()
+    dc.record_table(["sum"])
+    with pytest.raises(AssertionError):
+        census.assert_disjoint_cover("rows/sum", 64)
+    # and a multi-window sweep counts each window's rows in its own block
+    from paper_2410_16291_b200 import _device, _engine, _lib
+    import ctypes
+
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    x = to_dev(v)
+    sat, _, ld = _engine.build_tables(x, sb.ElemKind.U8, 64, 80, dev, squared=False)
+    ws = [5, 9]
+    outs = [_device.empty((64 - w + 1, 80 - w + 1), np.uint64, dev, "o") for w in ws]
+    cnt = torch.zeros(sum(64 - w + 1 for w in ws), dtype=torch.int64, device=dev)
+    _lib.check(lib.ssb_census_enable(None, 0, None, 0, cnt.data_ptr(), cnt.numel()))
+    arr = lambda t, vals: (t * 2)(*vals)  # noqa: E731
+    _lib.check(lib.ssb_window_eval_multi(sat.data_ptr(), None, _lib.U8, 64, 80, ld, 2, arr(ctypes.c_int64, ws), _lib.SUM,
+                                         arr(ctypes.c_void_p, [o.data_ptr() for o in outs]), None, None,
+                                         arr(ctypes.c_int64, [80 - w + 1 for w in ws]), _device.stream_ptr(dev)))
+    lib.ssb_census_disable()
+    c = cnt.cpu().numpy()
+    assert (c[:60] == 76).all() and (c[60:] == 72).all()
+
+
 def test_host_streaming_bands(sb):
     """ssb_swa_host with several bands equals one-shot evaluation (offsets cancel per band)."""
     from paper_2410_16291_b200 import _engine
@@ -514,3 +581,23 @@ def test_division_by_n_is_ieee(sb):
         _lib.check(lib.ssb_selftest_division(x.data_ptr(), x.numel(), float(n), bad.data_ptr(), st))
     torch.cuda.synchronize()
     assert int(bad.item()) == 0
+
+
+@pytest.mark.parametrize("w", [9, 64, 300])
+def test_float_methods_agree_bitwise(sb, w):
+    """Every entry point routes a float window the same way (the fused kernel
+    for stride 1, w <= 256; the table otherwise), so swa / swa_integral /
+    swa_parallel / multi_window agree bit for bit, as the reference's methods
+    do (SPEC.md:243-248; pkg/tests/test_api.py:68-79)."""
+    rng = np.random.default_rng(w)
+    v = rng.lognormal(0.0, 1.0, (700, 900)).astype(np.float32)
+    img = sb.ImageGrid(v)
+    for stat in ("sum", "mean", "std"):
+        a = sb.swa(v, w, stat)
+        b = sb.swa_integral(img, sb.WindowSpec(w), sb.StatKind(stat)).values
+        c = sb.swa_parallel(img, sb.WindowSpec(w), sb.StatKind(stat)).values
+        d = sb.multi_window(v, [5, w, 301], stat)[1]
+        e = sb.swa(to_dev(v), w, stat).cpu().numpy()
+        for other in (b, c, d, e):
+            np.testing.assert_array_equal(a, other)
+        np.testing.assert_allclose(a, O.swa(v, w, stat), rtol=1e-6, atol=0)
