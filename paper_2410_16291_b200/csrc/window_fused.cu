@@ -630,7 +630,8 @@ bool launch_strip(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* no
   // 4-byte elements with wide windows: 512-column strips (16 per lane), so the
   // w-1 halo columns cost less than with 256 (C2: w=100, C4: w=64)
   if constexpr (sizeof(InT) == 4) {
-    if (g.w > 48 && 32 * 2 * E1 - g.w + 1 >= 64) {
+    static const bool wide = env_int("SSB_FUSED_WIDE", 1) != 0;  // tuning: 0 keeps 256-column strips
+    if (wide && g.w > 48 && 32 * 2 * E1 - g.w + 1 >= 64) {
       // the BASELINE stat sets get a compile-time mask: C4 mean + std, C2 sum + mean
       if (kFloat_v<InT> && SQ && g.mask == (ST_MEAN | ST_STD))
         err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, false, ST_MEAN | ST_STD>(in, g, o, fi, nonfinite, nK, st);

@@ -143,7 +143,11 @@ class _DeviceCensus:
             i += 1
 
     def record_table(self, suffixes) -> None:
+        """Table phases; nothing when no table was written (float windows that
+        take the fused kernel, _engine.float_fused, never build one)."""
         pr, pc = self.img.rows + 1, self.img.cols + 1
+        if not self.counts["trow"].any() and not self.counts["tcol"].any():
+            return
         for sfx in suffixes:
             self.record(f"rows/{sfx}", "trow", pc, skip=1)
             self.record(f"cols/{sfx}", "tcol", pr, skip=1)
