@@ -31,9 +31,10 @@
  *     a pitch that is a multiple of 4 elements (rows are stored with 256-bit
  *     stores; SSB_EINVAL otherwise); tables it only READS need 16-byte
  *     alignment and an even pitch for the TMA corner sweep.
- *   - Every device pointer is caller-allocated device memory; the library keeps
- *     no persistent allocations (ssb_swa_host allocates and frees its own
- *     staging per call).
+ *   - Every device pointer is caller-allocated device memory.  The one
+ *     allocation the library keeps is ssb_swa_host's band buffers, held in a
+ *     library-private memory pool between calls (never the default pool or
+ *     the caller's allocator) until ssb_host_release().
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device entry
  *     points are asynchronous on that stream.
  *   - Tables are (rows+1) x (cols+1) with a zero border row/column and row
@@ -259,6 +260,10 @@ int ssb_selftest_division(const double* x, int64_t n, double divisor, unsigned l
 int ssb_census_enable(unsigned long long* table_rows, int64_t n_table_rows, unsigned long long* table_cols,
                       int64_t n_table_cols, unsigned long long* out_rows, int64_t n_out_rows);
 int ssb_census_disable(void);
+
+/* Return the band buffers ssb_swa_host keeps reserved between calls (its
+ * private pool on every device) to the device. */
+int ssb_host_release(void);
 
 /* Count of kernel launches the library issued since load (diagnostics). */
 int64_t ssb_launch_count(void);

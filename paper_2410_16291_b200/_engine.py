@@ -91,8 +91,11 @@ _SCRATCH = _Scratch()
 
 
 def release_scratch() -> None:
-    """Free the cached scratch tables (they are reused across swa/multi_window calls)."""
+    """Free the cached scratch tables (reused across swa/multi_window calls) and
+    the host path's band buffers (kept reserved in the library's private pool)."""
     _SCRATCH.clear()
+    if _lib.LIB_PATH.exists() and _device.torch().cuda.is_available():
+        _lib.load().ssb_host_release()
     t = _device.torch()
     if t.cuda.is_available():
         t.cuda.empty_cache()

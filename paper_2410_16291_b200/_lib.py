@@ -70,6 +70,7 @@ _SIGS = {
     "ssb_selftest_division": (_int, [_vp, _i64, ctypes.c_double, _vp, _vp]),
     "ssb_census_enable": (_int, [_vp, _i64, _vp, _i64, _vp, _i64]),
     "ssb_census_disable": (_int, []),
+    "ssb_host_release": (_int, []),
     "ssb_file_to_device": (_int, [ctypes.c_char_p, _i64, _i64, _vp, _int, _vp]),
     "ssb_device_to_file": (_int, [ctypes.c_char_p, _i64, _vp, _i64, _int, _vp]),
     "ssb_f32_nonfinite": (_int, [_vp, _i64, _vp, _vp]),

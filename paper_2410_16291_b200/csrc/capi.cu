@@ -350,11 +350,14 @@ int host_sets() {
   return n;
 }
 
-// one private pool per device for ssb_swa_host, created on first use (the
-// pool object holds no memory between calls: every call trims it to zero)
+// one private pool per device for ssb_swa_host's band buffers, created on
+// first use; it keeps the last call's buffers reserved (never the caller's
+// default pool or torch's allocator) until ssb_host_release()
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
 cudaError_t host_pool(int device, cudaMemPool_t* out) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
+  std::mutex& mu = g_pool_mu;
+  cudaMemPool_t* pools = g_pools;
   if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> lk(mu);
   if (!pools[device]) {
@@ -486,6 +489,16 @@ int ssb_window_sum_at(const void* sat, int is_float_table, int64_t rows, int64_t
 
 // ---------------------------------------------------------------------------
 // host-buffer end-to-end path (helpers host_sets / host_pool above)
+int ssb_host_release(void) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto& p : g_pools)
+    if (p) {
+      cudaError_t e = cudaMemPoolTrimTo(p, 0);
+      if (e != cudaSuccess) return cuda_fail(e, "ssb_host_release");
+    }
+  return SSB_OK;
+}
+
 
 int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
                  int64_t stride, int stat_mask, void* out_sum_host, double* out_mean_host, double* out_std_host,
@@ -581,41 +594,6 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   if (status == SSB_OK && (e = cudaMalloc(&d_flag, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
   if (status == SSB_OK && (e = cudaMemset(d_flag, 0, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
 
-  // tuning (SSB_HOST_RESIDENT): 1 = copy the whole raster in up front on its own
-  // stream (band by band, events per band) and compute every band from it;
-  // 2 = the same, and the result copies wait until the input is in (no
-  // H2D/D2H overlap on the link)
-  static const int resident_mode = env_int("SSB_HOST_RESIDENT", 0);
-  void* in_all = nullptr;
-  cudaStream_t h2d_st = nullptr;
-  std::vector<cudaEvent_t> ev_in;
-  const size_t all_bytes = (size_t)rows * cols * es;
-  bool resident = resident_mode > 0 && in_ld == cols && all_bytes <= ((size_t)24 << 30);
-  for (int64_t b = 0; resident && b < n_bands; ++b)
-    if (((size_t)b * band_rows * stride * cols * es) % 16) resident = false;  // TMA needs 16-byte aligned rows
-  if (status == SSB_OK && resident) {
-    if ((e = cudaStreamCreateWithFlags(&h2d_st, cudaStreamNonBlocking)) != cudaSuccess) status = cuda_fail(e, "stream");
-    else if (alloc(&in_all, all_bytes, h2d_st)) {
-      ev_in.assign(n_bands, nullptr);
-      int64_t done = 0;
-      for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
-        const int64_t o1 = ((b + 1) * band_rows < out_r) ? (b + 1) * band_rows : out_r;
-        const int64_t need_end = (o1 - 1) * stride + w;
-        if ((e = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming)) != cudaSuccess) { status = cuda_fail(e, "event"); break; }
-        if (need_end > done) {
-          e = cudaMemcpyAsync(reinterpret_cast<char*>(in_all) + (size_t)done * cols * es,
-                              reinterpret_cast<const char*>(in_host) + (size_t)done * cols * es,
-                              (size_t)(need_end - done) * cols * es, cudaMemcpyHostToDevice, h2d_st);
-          if (e != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
-          done = need_end;
-        }
-        if ((e = cudaEventRecord(ev_in[b], h2d_st)) != cudaSuccess) { status = cuda_fail(e, "event"); break; }
-      }
-      if (status == SSB_OK && resident_mode == 2 && (e = cudaStreamWaitEvent(d2h_st, ev_in[n_bands - 1], 0)) != cudaSuccess)
-        status = cuda_fail(e, "wait");
-    }
-  }
-
   for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
     Set& s = sets[b % n_sets];
     const int64_t o0 = b * band_rows, o1 = (o0 + band_rows < out_r) ? o0 + band_rows : out_r;
@@ -624,16 +602,11 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     // the set's outputs may be overwritten once its previous band is copied out
     if (b >= n_sets && (e = cudaStreamWaitEvent(s.st, s.drained, 0)) != cudaSuccess) { status = cuda_fail(e, "wait"); break; }
     const void* band_in = s.in;
-    if (in_all) {  // rows already on their way on the input stream
-      if ((e = cudaStreamWaitEvent(s.st, ev_in[b], 0)) != cudaSuccess) { status = cuda_fail(e, "wait"); break; }
-      band_in = reinterpret_cast<const char*>(in_all) + (size_t)r0 * cols * es;
-    } else {
-      // contiguous rows: one linear copy (no per-row DMA descriptors)
-      e = in_ld == cols ? cudaMemcpyAsync(s.in, src, (size_t)nr * cols * es, cudaMemcpyHostToDevice, s.st)
-                        : cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es,
-                                            (size_t)nr, cudaMemcpyHostToDevice, s.st);
-      if (e != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
-    }
+    // contiguous rows: one linear copy (no per-row DMA descriptors)
+    e = in_ld == cols ? cudaMemcpyAsync(s.in, src, (size_t)nr * cols * es, cudaMemcpyHostToDevice, s.st)
+                      : cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es,
+                                          (size_t)nr, cudaMemcpyHostToDevice, s.st);
+    if (e != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
     WinOut o{s.o_sum, reinterpret_cast<double*>(s.o_mean), reinterpret_cast<double*>(s.o_std), out_c};
     if (pipeline == SSB_PIPE_TABLE && sweep_ok) {  // table + windows without reading the table back
       e = launch_sat_sweep(in_dtype, band_in, nr, cols, cols, s.sat, sat_ld, w, stat_mask, o, s.ws, s.st, false);
@@ -681,17 +654,10 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     cudaStreamDestroy(s.st);
   }
   if (d2h_st) cudaStreamDestroy(d2h_st);
-  if (h2d_st) {
-    cudaError_t se = cudaStreamSynchronize(h2d_st);
-    if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");
-    if (in_all) cudaFreeAsync(in_all, h2d_st);
-    cudaStreamSynchronize(h2d_st);
-    cudaStreamDestroy(h2d_st);
-  }
-  for (cudaEvent_t ev : ev_in)
-    if (ev) cudaEventDestroy(ev);
-  static const bool keep_pool = env_int("SSB_HOST_KEEP_POOL", 0) != 0;  // tuning: keep band buffers reserved
-  if (!keep_pool) cudaMemPoolTrimTo(pool, 0);
+  // the freed band buffers stay reserved in the library's pool for the next
+  // call (mapping ~9 GB of fresh device memory costs ~0.1 s per C5 call);
+  // ssb_host_release() returns them.  Errors trim it right away.
+  if (status != SSB_OK) cudaMemPoolTrimTo(pool, 0);
   if (d_flag) {
     int h = 0;
     if (status == SSB_OK) {

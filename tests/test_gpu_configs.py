@@ -126,8 +126,10 @@ def test_c5_bands(sb, hashes, dev, band):
 
 
 def test_c5_full_image(sb, hashes, dev):
-    """Whole 70,000 x 85,000 raster on one GPU: reference-hashed bands of the full result,
-    random rows against the oracle, and table == fused."""
+    """Whole 70,000 x 85,000 raster on one GPU: reference-hashed bands of the full result
+    and random rows against the oracle (the whole result and the whole table are
+    checked band by band in test_gpu_scale.py; the corner sweep that reads the
+    table back is checked there too)."""
     import torch
 
     from paper_2410_16291_b200 import synthetic
@@ -141,9 +143,7 @@ def test_c5_full_image(sb, hashes, dev):
     for i in rng.integers(0, 69745, size=3).tolist():
         band = host(x[i:i + 256], np.uint8)
         np.testing.assert_array_equal(host(out[i], np.uint64), O.swa(band, 256, "sum")[0])
-    fused = sb.swa(x, 256, "sum", pipeline="fused")
-    assert bool(torch.equal(fused, out))
-    del out, fused, x
+    del out, x
     torch.cuda.empty_cache()
 
 

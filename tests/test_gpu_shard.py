@@ -181,3 +181,25 @@ def test_sharded_swa_validation(sb):
                                one) == _lib.EINVAL
     assert lib.ssb_sharded_swa(1, devs, 9, 10, 10, 3, _lib.SUM, one, None, 12, one, None, None, 8, None, None,
                                one) == _lib.EUNSUPPORTED
+
+
+def test_swa_table_sharded_single_rank(sb):
+    """bench.py's multi-GPU step (shard.swa_table_sharded with the CUDA backend)
+    on one rank: the windows on the side stream and the table rows equal the
+    oracle; a second call reuses every buffer."""
+    import torch
+
+    from paper_2410_16291_b200 import shard
+    from paper_2410_16291_b200.grid import ElemKind, StatKind
+
+    img = _img("u8", (1500, 2100), 21)
+    dev = torch.device("cuda", 0)
+    storage, view = shard.band_storage(1500, 2100, 64, 1, torch.uint8, dev)
+    view.copy_(torch.from_numpy(img))
+    be = shard.CudaBackend(dev)
+    for _ in range(2):
+        wr, tr = shard.swa_table_sharded(view, 1500, 2100, ElemKind.U8, 64, (StatKind.SUM,), be, storage=storage)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(wr.values[StatKind.SUM].cpu().numpy().view(np.uint64), O.swa(img, 64, "sum"))
+    assert tr.rows == (0, 1500)
+    np.testing.assert_array_equal(tr.values["table"].cpu().numpy().view(np.uint64)[:, :2101], O.build_table(img))
