@@ -191,6 +191,36 @@ def fused(x, kind: ElemKind, rows: int, cols: int, w: int, stats, device, flag=N
     return outs
 
 
+_SIDE: dict = {}
+
+
+def _side_streams(device, n: int):
+    t = _device.torch()
+    key = str(device)
+    cur = _SIDE.setdefault(key, [])
+    while len(cur) < n:
+        cur.append(t.cuda.Stream(device))
+    return cur[:n]
+
+
+def fused_windows(x, kind: ElemKind, rows: int, cols: int, windows, stats, device, flag=None):
+    """Several stride-1 windows without a table, each on its own stream forked
+    from (and joined back into) the current one, so the launches overlap and
+    fill each other's tails.  Returns one {StatKind: tensor} per window."""
+    t = _device.torch()
+    cur = t.cuda.current_stream(device)
+    outs = [alloc_outputs(kind, stats, rows - w + 1, cols - w + 1, device) for w in windows]
+    sides = _side_streams(device, len(windows))
+    for st in sides:
+        st.wait_stream(cur)
+    for w, o, st in zip(windows, outs, sides):
+        with t.cuda.stream(st):
+            fused(x, kind, rows, cols, w, stats, device, flag=flag, outs=o)
+    for st in sides:
+        cur.wait_stream(st)
+    return outs
+
+
 def fused_max_w() -> int:
     return int(_lib.load().ssb_window_fused_max_w())
 

@@ -117,4 +117,15 @@ def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str 
     if pipeline in ("auto", "table"):
         grid = img if img.on_device else ImageGrid(img.values, img.elem_kind, _check_finite=False)
         return [r.values for r in _run_tables(grid, specs, kind, force_table=pipeline == "table")]
-    return [swa(array, s.w, kind.value, pipeline="fused") for s in specs]
+    if max(windows) > _engine.fused_max_w():
+        raise ValueError("the fused pipeline needs w <= %d" % _engine.fused_max_w())
+    # fused: every window from the raster, the launches on concurrent streams
+    with _engine.on_device(img):
+        x, dev = _engine.device_input(img)
+        flag = _engine.new_flag(dev) if img.elem_kind.value == "f32" else None
+        res = _engine.fused_windows(x, img.elem_kind, img.rows, img.cols, list(windows), [kind], dev, flag=flag)
+        _engine.check_nonfinite(flag)
+        out = [r[kind] for r in res]
+        if not img.on_device:
+            out = [_engine._device.to_host(o, _engine.result_dtype(img.elem_kind, kind)) for o in out]
+        return out

@@ -591,6 +591,8 @@ cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   using SM = StripSmem<InT, E, RB, VT, VQ, SQ>;
   g.two = SM::NV - g.w + 1;
   const int nJ = (int)((g.out_c + g.two - 1) / g.two);
+  static const int env_k = env_int("SSB_FUSED_SEGMENTS", 0);  // tuning: row segments per strip
+  if (nK_override <= 0 && env_k > 0) nK_override = env_k;
   int64_t nK = nK_override > 0 ? nK_override : (int64_t)(2 * kNumSMs * 12 + nJ - 1) / nJ;
   if (nK > g.out_r) nK = g.out_r;
   if (nK < 1) nK = 1;
@@ -608,166 +610,6 @@ cudaError_t launch_strip_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   const int64_t warps = (int64_t)nJ * nK;
   const int blocks = (int)((warps + kStripWarps - 1) / kStripWarps);
   kfn<<<blocks, 32 * kStripWarps, smem, st>>>(reinterpret_cast<const InT*>(in), g, o, fi, nJ, (int)nK, nonfinite);
-  note_launch(1);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Warp-pair kernel for float windows with std (C4: mean + std).  The strip
-// kernel keeps both vertical sums (V and V of squares, 2 x 16 doubles per
-// lane) live in one warp: ~166 registers, 12 warps per SM, latency-bound.
-// Here the two running sums of a strip live in two warps of a pair that share
-// one TMA ring: role 0 accumulates x, role 1 accumulates x^2 -- the same
-// instruction stream (FMA with 1 or with x; x^2 of a float is exact in double,
-// so each role rounds once per update) -- and each publishes its row prefix
-// (P or Pq) into a double-buffered smem row; one named barrier per row, then
-// both warps finalize half of the row's outputs each from P and Pq.
-constexpr int kPairCta = 2;  // pairs (warp pairs) per CTA
-
-template <int E>
-struct PairSmem {
-  static constexpr int NV = 32 * E;
-  static constexpr int ROWB = NV * 4 + 48;
-  static constexpr int NSTG = 2;
-  alignas(16) unsigned char stage[NSTG][2][ROWB];  // [stage][entering, leaving row]
-  int offs[NSTG][2];
-  uint64_t bar[NSTG];
-  double p[2][NV + 72];   // P of row parity 0/1, P[u] at word u + u / 32
-  double pq[2][NV + 72];
-};
-
-__device__ __forceinline__ void pair_sync(int pair) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-}
-
-template <int E, int MASKT>
-__global__ void __launch_bounds__(64 * kPairCta, 4)
-fused_pair_kernel(const float* __restrict__ in, FusedGeom g, WinOut o, FinalizeInt fi, int nJ, int nK,
-                  int* __restrict__ nonfinite) {
-  using SM = PairSmem<E>;
-  constexpr int NV = SM::NV, ES = 4, NW = E;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pair = warp >> 1, role = warp & 1;
-  SM& sm = reinterpret_cast<SM*>(smem_raw)[pair];
-  const int t = blockIdx.x * kPairCta + pair;
-  if (t >= nJ * nK) return;  // both warps of the pair leave together
-  const int J = t % nJ, K = t / nJ;
-  const int w = g.w;
-  const int64_t oc0 = (int64_t)J * g.two;
-  const int nout = (int)min64(g.two, g.out_c - oc0);
-  const int64_t or0 = (int64_t)K * g.sro, or1 = min64(or0 + g.sro, g.out_r);
-  if (nout <= 0 || or0 >= or1) return;
-  const int64_t r_beg = or0, r_end = or1 + w - 1;
-  const int nblk = (int)(r_end - r_beg);
-  const int64_t c_lo = oc0, c_hi = min64(oc0 + NV, g.C);
-  const int64_t c0 = oc0 + lane * E;
-  const char* base = reinterpret_cast<const char*>(in);
-  const char* end_valid = base + ((g.R - 1) * g.in_ld + g.C) * ES;
-  if (role == 0 && lane == 0) {
-    for (int i = 0; i < SM::NSTG; ++i) mbar_init(&sm.bar[i], 1);
-    fence_mbar_init();
-  }
-  pair_sync(pair);
-  // role 0, lane 0 stages entering row rb, lane 1 leaving row rb - w
-  auto issue = [&](int b, int st) {
-    const int64_t rb = r_beg + b;
-    const bool old = lane == 1;
-    const int64_t r = rb - (old ? w : 0);
-    const bool has = lane < 2 && rb < r_end && (!old || rb - w >= r_beg);
-    unsigned char* dst = sm.stage[st][lane < 2 ? lane : 0];
-    RowSpan sp;
-    if (has) sp = row_span(base + r * g.in_ld * ES, c_lo, c_hi, ES, end_valid, dst);
-    if (lane < 2) sm.offs[st][lane] = has ? sp.off : kNoRow;
-    warp_issue(sp, has, dst, &sm.bar[st], lane);
-  };
-  if (role == 0)
-    for (int b = 0; b < SM::NSTG - 1; ++b)
-      if (b < nblk) issue(b, b);
-
-  double A[E];  // role 0: window sums of x; role 1: of x^2
-#pragma unroll
-  for (int k = 0; k < E; ++k) A[k] = 0.0;
-  bool nf = false;
-  const int ubase = lane * E + 1;
-  const int addr_a = lane;
-  const int addr_b = lane + w + ((lane + w) >> 5);
-  const int mk = MASKT != 0 ? MASKT : g.mask;
-
-  for (int b = 0; b < nblk; ++b) {
-    const int st = b % SM::NSTG;
-    // the stage refilled here was read by both warps in iteration b - 1,
-    // before the pair barrier both have passed
-    if (role == 0 && b + SM::NSTG - 1 < nblk) issue(b + SM::NSTG - 1, (b + SM::NSTG - 1) % SM::NSTG);
-    mbar_wait(&sm.bar[st], (uint32_t)((b / SM::NSTG) & 1));
-    const int64_t r = r_beg + b;
-    {
-      uint32_t oo[NW], on[NW];
-      lane_elems_packed<float, E>(sm.stage[st][1], sm.offs[st][1], c0, g.C, oo);
-      lane_elems_packed<float, E>(sm.stage[st][0], sm.offs[st][0], c0, g.C, on);
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        const double xo = (double)elem<float>(oo, k), xn = (double)elem<float>(on, k);
-        A[k] = __fma_rn(-xo, role ? xo : 1.0, A[k]);  // - xo * (role ? xo : 1): exact product, one rounding
-        A[k] = __fma_rn(xn, role ? xn : 1.0, A[k]);
-        nf |= is_nonfinite(elem<float>(on, k));
-      }
-    }
-    const bool emit = r >= r_beg + w - 1;
-    const int buf = b & 1;
-    if (emit) {
-      double* P = role ? sm.pq[buf] : sm.p[buf];
-      double run = warp_excl_scan(tree_sum<E, double>([&](int k) { return A[k]; }), lane);
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        run += A[k];
-        const int u = ubase + k;
-        P[u + (u >> 5)] = run;
-      }
-      if (lane == 0) P[0] = 0.0;
-    }
-    pair_sync(pair);
-    if (!emit) continue;
-    const int64_t i = r - (w - 1);
-    const double* P = sm.p[buf];
-    const double* Q = sm.pq[buf];
-    // outputs j = lane + 32 q: role 0 takes even q, role 1 odd q
-    const int nq = (nout - lane + 31) >> 5;
-    const int64_t obase = i * o.ld + oc0 + lane + 32 * role;
-    double* p_sum = reinterpret_cast<double*>(o.sum) + obase;
-    double* p_mean = o.mean + obase;
-    double* p_std = o.std_ + obase;
-    int a = addr_a + 33 * role, bw = addr_b + 33 * role;
-    for (int qq = role; qq < nq; qq += 2, a += 66, bw += 66, p_sum += 64, p_mean += 64, p_std += 64) {
-      const double sv = P[bw] - P[a];
-      const double qv = Q[bw] - Q[a];
-      if (mk & ST_SUM) st_cs(p_sum, sv);
-      if (mk & ST_MEAN) st_cs(p_mean, fin_mean_f(sv, fi.dn, fi.inv_n));
-      if (mk & ST_STD) st_cs(p_std, fin_std_f(sv, qv, fi.dn, fi.inv_n));
-      census_add(g.cz.orow, g.cz.nor, i);
-    }
-  }
-  if (nf && nonfinite) atomicOr(nonfinite, 1);
-}
-
-template <int E, int MASKT>
-cudaError_t launch_pair_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* nonfinite, int nK_override,
-                          cudaStream_t st) {
-  using SM = PairSmem<E>;
-  g.two = SM::NV - g.w + 1;
-  const int nJ = (int)((g.out_c + g.two - 1) / g.two);
-  int64_t nK = nK_override > 0 ? nK_override : (int64_t)(kNumSMs * 4 * kPairCta * 3 + nJ - 1) / nJ;
-  if (nK > g.out_r) nK = g.out_r;
-  if (nK < 1) nK = 1;
-  g.sro = (g.out_r + nK - 1) / nK;
-  nK = (g.out_r + g.sro - 1) / g.sro;
-  auto kfn = fused_pair_kernel<E, MASKT>;
-  const size_t smem = sizeof(SM) * kPairCta;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int64_t pairs = (int64_t)nJ * nK;
-  const int blocks = (int)((pairs + kPairCta - 1) / kPairCta);
-  kfn<<<blocks, 64 * kPairCta, smem, st>>>(reinterpret_cast<const float*>(in), g, o, fi, nJ, (int)nK, nonfinite);
   note_launch(1);
   return cudaGetLastError();
 }
@@ -793,15 +635,6 @@ bool launch_strip(const void* in, FusedGeom g, WinOut o, FinalizeInt fi, int* no
     static const bool wide = env_int("SSB_FUSED_WIDE", 1) != 0;  // tuning: 0 keeps 256-column strips
     if (wide && g.w > 48 && 32 * 2 * E1 - g.w + 1 >= 64) {
       // the BASELINE stat sets get a compile-time mask: C4 mean + std, C2 sum + mean
-      static const bool pairs = env_int("SSB_FUSED_PAIR", 1) != 0;  // tuning: 0 = single-warp strips
-      if constexpr (kFloat_v<InT> && SQ) {
-        if (pairs) {
-          err = g.mask == (ST_MEAN | ST_STD)
-                    ? launch_pair_t<2 * E1, ST_MEAN | ST_STD>(in, g, o, fi, nonfinite, nK, st)
-                    : launch_pair_t<2 * E1, 0>(in, g, o, fi, nonfinite, nK, st);
-          return true;
-        }
-      }
       if (kFloat_v<InT> && SQ && g.mask == (ST_MEAN | ST_STD))
         err = launch_strip_t<InT, 2 * E1, VT, VQ, SQ, false, ST_MEAN | ST_STD>(in, g, o, fi, nonfinite, nK, st);
       else if (!SQ && g.mask == (ST_SUM | ST_MEAN))
