@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _engine
+from . import _device, _engine
 from .grid import ImageGrid, StatKind, WindowSpec, _is_torch
 
 METHODS = ("naive", "dp", "integral", "parallel")
@@ -127,5 +127,5 @@ def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str 
         _engine.check_nonfinite(flag)
         out = [r[kind] for r in res]
         if not img.on_device:
-            out = [_engine._device.to_host(o, _engine.result_dtype(img.elem_kind, kind)) for o in out]
+            out = [_device.to_host(o, _engine.result_dtype(img.elem_kind, kind)) for o in out]
         return out

@@ -1,0 +1,274 @@
+// satsweep-b200: the integral image AND its window sums in one persistent
+// column-strip sweep (uint8 rasters, w <= 256): the headline step of
+// ssb_sat_build_swa.
+//
+// Same products as build_sat + sweep_window_sums (pkg/src/satsweep/integral.py
+// :109-116, :141-163): the (R+1) x (C+1) uint64 table and the window sums, bit
+// for bit.  Why a new kernel: the concurrent pair (reduce-then-scan build ||
+// fused windows, sat_sweep.cu) moves 121.7 GB for the 100.8 GB the step needs
+// -- the raster is read by the reduce, the scan, and twice by the window kernel
+// (rows r and r-w), because ~1,800 warps each sweep their own short segment,
+// so the w-row history behind them is ~1 GB, far beyond L2.
+//
+// Here each CTA owns one 576-column strip of the table (+ 320 halo columns for
+// the windows) and sweeps ALL rows top to bottom, 16 rows per step:
+//   * the history behind the CTAs is 148 strips x w rows x 896 bytes = 32 MB,
+//     so the leaving rows (r - w) come back from L2 (raster rows are fetched
+//     with an evict_last policy, leaving rows with evict_first, the 95 GB of
+//     table and window stores stream past as evict-first);
+//   * no top carries: a column's running table value stays in the thread that
+//     owns it for the whole height;
+//   * left carries (the row's total left of the strip) come from a small
+//     pre-pass (strip_carry_kernel: one read of the raster, 41 MB of u32
+//     carries at C5), so no CTA ever waits on another.
+// Per step: phase 1 (7 warps) updates the vertical window sums V of the 896
+// columns (two columns per 32-bit word as 16-bit halves, as in window_fused.cu)
+// and the 4-column byte sums of the table row segment; phase 2 (16 warps, one
+// row each) scans those sums across the strip and turns V into window sums
+// (packed_sums_row); phase 3 (144 threads, 4 table columns each) adds carry +
+// prefix to the column accumulators and stores the 16 table rows with 256-bit
+// stores.  Integer sums are exact modulo 2^64 in the same ring as the
+// reference's U64 table.
+#include <cstdint>
+
+#include "ssb_async.cuh"
+#include "ssb_common.cuh"
+#include "ssb_stage.cuh"
+#include "ssb_packed.cuh"
+
+namespace ssb {
+void note_launch(int n);
+
+constexpr int kStripCols = 576;                 // table columns per CTA
+constexpr int kStripSpan = 896;                 // raster columns per CTA (576 + halo, 28 per lane)
+constexpr int kStripRows = 16;                  // rows per step
+constexpr int kStripThreads = 512;              // 16 warps
+constexpr int kStripNS = 3;                     // TMA ring depth (steps in flight + 2)
+constexpr int kStripRowB = kStripSpan + 64;     // staged row: 16 pad + span + misalignment + tail
+constexpr int kStripVThreads = kStripSpan / 4;  // 224 threads own 4 columns each of V
+constexpr int kStripTThreads = kStripCols / 4;  // 144 threads own 4 table columns each
+constexpr int kStripPWords = 960;               // per-warp prefix buffer (packed_sums_row, pp() layout)
+
+struct StripSmem {
+  alignas(16) unsigned char stage[kStripNS][2 * kStripRows][kStripRowB];  // rows 0..15 new, 16..31 leaving
+  int offs[kStripNS][2 * kStripRows];
+  uint64_t bar[kStripNS];
+  uint32_t vs[kStripRows][2 * kStripVThreads];  // V of each row of the step (packed words)
+  uint32_t tot[kStripRows][kStripTThreads];     // 4-column byte sums of each row
+  uint32_t off[kStripRows][kStripTThreads];     // their exclusive prefix across the strip
+  uint32_t lx[kStripRows];                      // left carries of the step's rows
+  uint32_t pw[kStripThreads / 32][kStripPWords];
+};
+
+// ---- pre-pass: left carry of every (row, strip) -------------------------------
+// Lx[r][s] = sum of x[r][c] for c < 576 s (u32: at most 576 * 255 * strips).
+// One warp per row: lane l sums strips l, l + 32, ... with 8-byte loads
+// (in_ld % 8 == 0), then an exclusive scan across the strips.
+__global__ void __launch_bounds__(256) strip_carry_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C,
+                                                           int64_t in_ld, int nS, uint32_t* __restrict__ lx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += warps) {
+    const uint8_t* row = in + r * in_ld;
+    uint32_t carry = 0;
+    for (int s0 = 0; s0 < nS; s0 += 32) {
+      const int s = s0 + lane;
+      uint32_t tot = 0;
+      if (s < nS) {
+        const int64_t c0 = (int64_t)s * kStripCols;
+        const int64_t c1 = c0 + kStripCols < C ? c0 + kStripCols : C;
+        if (c1 - c0 == kStripCols) {
+          const uint2* p = reinterpret_cast<const uint2*>(row + c0);
+#pragma unroll 8
+          for (int k = 0; k < kStripCols / 8; ++k) {
+            const uint2 v = __ldcs(p + k);
+            tot = __dp4a(v.x, 0x01010101u, tot);
+            tot = __dp4a(v.y, 0x01010101u, tot);
+          }
+        } else {
+          for (int64_t c = c0; c < c1; ++c) tot += row[c];
+        }
+      }
+      const uint32_t inc = warp_incl_scan(tot, lane);
+      if (s < nS) lx[r * nS + s] = carry + inc - tot;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+}
+
+// 4 raster bytes at byte position p of a staged row (any alignment)
+__device__ __forceinline__ uint32_t row_word(const unsigned char* rowbuf, int p) {
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(rowbuf);
+  const int q = p >> 2;
+  return __funnelshift_r(wd[q], wd[q + 1], (p & 3) * 8);
+}
+
+__global__ void __launch_bounds__(kStripThreads, 1)
+sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t in_ld, uint64_t* __restrict__ sat,
+                 int64_t sat_ld, uint64_t* __restrict__ out, int64_t out_ld, int64_t out_c, int w,
+                 const uint32_t* __restrict__ lx, int nS, Census cz) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StripSmem& sm = *reinterpret_cast<StripSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = blockIdx.x;
+  const int64_t c0 = (int64_t)s * kStripCols;  // first table column = first raster column of the span
+  const int64_t PC = C + 1;
+  const int64_t out_r = R - w + 1;
+  const int nout = (int)(out_c - c0 < kStripCols ? out_c - c0 : kStripCols);
+  const int nsteps = (int)((R + kStripRows - 1) / kStripRows);
+  const char* base = reinterpret_cast<const char*>(in);
+  const char* end_valid = base + (R - 1) * in_ld + C;
+  const int64_t c_hi = c0 + kStripSpan < C ? c0 + kStripSpan : C;
+  if (tid == 0) {
+    for (int i = 0; i < kStripNS; ++i) mbar_init(&sm.bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // producer: warp 15, lane q < 16 stages new row r0 + q, lane 16 + q the leaving row r0 + q - w
+  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+  auto issue = [&](int b, int st) {
+    const int64_t r0 = (int64_t)b * kStripRows;
+    const int q = lane & (kStripRows - 1);
+    const bool old = lane >= kStripRows;
+    const int64_t r = r0 + q - (old ? w : 0);
+    const bool has = r0 + q < R && r >= 0;
+    unsigned char* dst = sm.stage[st][lane];
+    RowSpan sp;
+    if (has) sp = row_span(base + r * in_ld, c0, c_hi, 1, end_valid, dst);
+    sm.offs[st][lane] = has ? sp.off : kNoRow;
+    warp_issue_hint(sp, has, dst, &sm.bar[st], lane, old ? drop : keep);
+  };
+  if (warp == 15)
+    for (int b = 0; b < kStripNS - 1; ++b)
+      if (b < nsteps) issue(b, b);
+
+  // phase-1 state: V words of columns 4t..4t+3 (t < 224)
+  uint32_t V0 = 0u, V1 = 0u;
+  // phase-3 state: table accumulators of columns c0 + 4t .. +3 (t < 144)
+  uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+  uint32_t xw[kStripRows];  // the 4 new bytes of every row of the step (t < 144)
+  const int64_t tc = c0 + 4 * tid;  // table column of this thread's first accumulator
+  const bool tab = tid < kStripTThreads && tc < PC;
+  if (tab) {  // table row 0: the zero border
+    const U64x4 z{0ull, 0ull, 0ull, 0ull};
+    if (tc + 4 <= PC) st256(sat + tc, z);
+    else for (int k = 0; k < 4; ++k) if (tc + k < PC) st_cs(sat + tc + k, (uint64_t)0);
+    if (cz.trow != nullptr)
+      for (int k = 0; k < 4; ++k)
+        if (tc + k < PC) { census_add(cz.trow, cz.ntr, 0); census_add(cz.tcol, cz.ntc, tc + k); }
+  }
+
+  for (int b = 0; b < nsteps; ++b) {
+    const int st = b % kStripNS;
+    const int64_t r0 = (int64_t)b * kStripRows;
+    // the stage refilled here was released by the last barrier of step b - 1
+    if (warp == 15 && b + kStripNS - 1 < nsteps) issue(b + kStripNS - 1, (b + kStripNS - 1) % kStripNS);
+    if (tid < kStripRows) sm.lx[tid] = r0 + tid < R ? lx[(r0 + tid) * nS + s] : 0u;
+    mbar_wait(&sm.bar[st], (uint32_t)((b / kStripNS) & 1));
+    // ---- phase 1: V update (224 threads) and 4-column byte sums (144 threads)
+    if (tid < kStripVThreads) {
+      const int64_t cc = c0 + 4 * tid;
+      // bytes past the raster's last column are zero (not in the staged span)
+      const uint32_t keepmask = cc + 4 <= C ? 0xFFFFFFFFu : cc >= C ? 0u : (0xFFFFFFFFu >> (8 * (4 - (int)(C - cc))));
+#pragma unroll
+      for (int g = 0; g < kStripRows; ++g) {
+        const int on = sm.offs[st][g], oo = sm.offs[st][kStripRows + g];
+        const uint32_t nw = on == kNoRow ? 0u : row_word(sm.stage[st][g], 16 + on + 4 * tid) & keepmask;
+        const uint32_t ow = oo == kNoRow ? 0u : row_word(sm.stage[st][kStripRows + g], 16 + oo + 4 * tid) & keepmask;
+        // V >= the leaving row in every column, so no borrow crosses a 16-bit half
+        V0 = V0 - (ow & 0x00FF00FFu) + (nw & 0x00FF00FFu);
+        V1 = V1 - ((ow >> 8) & 0x00FF00FFu) + ((nw >> 8) & 0x00FF00FFu);
+        sm.vs[g][2 * tid] = V0;
+        sm.vs[g][2 * tid + 1] = V1;
+        if (tid < kStripTThreads) {
+          xw[g] = nw;
+          sm.tot[g][tid] = __dp4a(nw, 0x01010101u, 0u);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: warp g owns row r0 + g
+    {
+      const int g = warp;
+      const int64_t r = r0 + g;
+      // (a) exclusive prefix of the 4-column sums across the strip
+      uint32_t carry = 0u;
+#pragma unroll
+      for (int k = 0; k < (kStripTThreads + 31) / 32; ++k) {
+        const int t = 32 * k + lane;
+        const uint32_t v = t < kStripTThreads ? sm.tot[g][t] : 0u;
+        const uint32_t inc = warp_incl_scan(v, lane);
+        if (t < kStripTThreads) sm.off[g][t] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      // (b) the window sums whose bottom row is r: output row r - (w - 1)
+      const int64_t i = r - (w - 1);
+      if (r < R && i >= 0 && i < out_r && nout > 0) {
+        uint32_t Vl[14];
+#pragma unroll
+        for (int k = 0; k < 14; ++k) Vl[k] = sm.vs[g][14 * lane + k];
+        packed_sums_row<28>(Vl, sm.pw[warp], i * out_ld + c0, out, nout, w, lane, cz, i);
+      }
+    }
+    __syncthreads();
+    // ---- phase 3: table rows r0 + 1 .. r0 + 16 (144 threads x 4 columns)
+    if (tab) {
+#pragma unroll
+      for (int g = 0; g < kStripRows; ++g) {
+        const int64_t r = r0 + g;
+        if (r >= R) break;
+        const uint32_t x = xw[g];
+        const uint32_t b0 = x & 0xFFu, b1 = (x >> 8) & 0xFFu, b2 = (x >> 16) & 0xFFu;
+        const uint64_t left = (uint64_t)sm.lx[g] + (uint64_t)sm.off[g][tid];
+        acc[0] += left;
+        acc[1] += left + b0;
+        acc[2] += left + b0 + b1;
+        acc[3] += left + b0 + b1 + b2;
+        uint64_t* dst = sat + (r + 1) * sat_ld + tc;
+        if (tc + 4 <= PC) {
+          const U64x4 v{acc[0], acc[1], acc[2], acc[3]};
+          st256(dst, v);
+        } else {
+          for (int k = 0; k < 4; ++k)
+            if (tc + k < PC) st_cs(dst + k, acc[k]);
+        }
+        if (cz.trow != nullptr)
+          for (int k = 0; k < 4; ++k)
+            if (tc + k < PC) { census_add(cz.trow, cz.ntr, r + 1); census_add(cz.tcol, cz.ntc, tc + k); }
+      }
+    }
+    __syncthreads();  // stage st, vs, tot, off and lx are reused
+  }
+}
+
+bool sat_strip_supported(int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask, int64_t sat_ld) {
+  // uint8 sums, w <= 256 (16-bit V halves), rasters wide enough to give every
+  // SM a strip, 8-byte aligned rows for the carry pre-pass
+  return dtype == IN_U8 && mask == ST_SUM && w <= 256 && C >= (int64_t)kNumSMs * kStripCols / 2 && R >= w &&
+         (in_ld % 8) == 0 && (sat_ld % 4) == 0 && C * 255 < ((int64_t)1 << 32);
+}
+
+int64_t sat_strip_workspace_bytes(int64_t R, int64_t C) {
+  const int64_t nS = (C + 1 + kStripCols - 1) / kStripCols;
+  return R * nS * 4 + 256;
+}
+
+cudaError_t launch_sat_strip(const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld, int64_t w,
+                             WinOut o, void* ws, cudaStream_t st) {
+  const int nS = (int)((C + 1 + kStripCols - 1) / kStripCols);
+  uint32_t* lx = reinterpret_cast<uint32_t*>(ws);
+  const int cblocks = (int)((R + 7) / 8 < 16 * kNumSMs ? (R + 7) / 8 : 16 * kNumSMs);
+  strip_carry_kernel<<<cblocks, 256, 0, st>>>(reinterpret_cast<const uint8_t*>(in), R, C, in_ld, nS, lx);
+  note_launch(1);
+  const size_t smem = sizeof(StripSmem);
+  cudaError_t e = cudaFuncSetAttribute(sat_strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  sat_strip_kernel<<<nS, kStripThreads, smem, st>>>(reinterpret_cast<const uint8_t*>(in), R, C, in_ld,
+                                                    reinterpret_cast<uint64_t*>(sat), sat_ld,
+                                                    reinterpret_cast<uint64_t*>(o.sum), o.ld, C - w + 1, (int)w, lx,
+                                                    nS, census_sink());
+  note_launch(1);
+  return cudaGetLastError();
+}
+
+}  // namespace ssb

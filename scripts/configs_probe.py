@@ -17,8 +17,28 @@ CASES = {
 }
 
 
+def c3(pipe, steps):
+    x = torch.from_numpy(synthetic.c3()).to("cuda:0")
+    ws = [25, 50, 100, 200, 400]
+    for _ in range(2):
+        sb.multi_window(x, ws, "sum", pipeline=pipe)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        sb.multi_window(x, ws, "sum", pipeline=pipe)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    floor = 30000 * 30000 + sum((30000 - w + 1) ** 2 * 8 for w in ws)
+    print(json.dumps({"config": "C3", "pipeline": pipe, "ms": ms, "floor_GB": floor / 1e9,
+                      "floor_frac": floor / (ms * 1e-3) / 6554.6e9}), flush=True)
+
+
 def main():
     name, pipe = sys.argv[1], sys.argv[2]
+    if name == "C3":
+        return c3(pipe, int(sys.argv[3]) if len(sys.argv) > 3 else 10)
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
     gen, w, stats = CASES[name]
     x = torch.from_numpy(gen()).to("cuda:0")
