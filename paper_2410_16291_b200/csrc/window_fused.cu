@@ -19,6 +19,7 @@
 
 #include "ssb_common.cuh"
 #include "ssb_stage.cuh"
+#include "ssb_packed.cuh"
 
 #ifndef SSB_FUSED_LOAD_HINT
 #define SSB_FUSED_LOAD_HINT 0
@@ -253,8 +254,6 @@ cudaError_t launch_fused_t(const void* in, FusedGeom g, WinOut o, FinalizeInt fi
   note_launch(1);
   return cudaGetLastError();
 }
-
-#include "ssb_packed.cuh"
 
 // ---------------------------------------------------------------------------
 // Strip kernel (default).  Every warp owns one output-column strip of TWo = NV
