@@ -173,8 +173,9 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
 #pragma unroll
       for (int g = 0; g < kStripRows; ++g) {
         const int on = sm.offs[st][g], oo = sm.offs[st][kStripRows + g];
-        const uint32_t nw = on == kNoRow ? 0u : row_word(sm.stage[st][g], 16 + on + 4 * tid) & keepmask;
-        const uint32_t ow = oo == kNoRow ? 0u : row_word(sm.stage[st][kStripRows + g], 16 + oo + 4 * tid) & keepmask;
+        // image column c sits at byte 16 + off + c of a staged row (ssb_stage.cuh)
+        const uint32_t nw = on == kNoRow ? 0u : row_word(sm.stage[st][g], 16 + on + (int)cc) & keepmask;
+        const uint32_t ow = oo == kNoRow ? 0u : row_word(sm.stage[st][kStripRows + g], 16 + oo + (int)cc) & keepmask;
         // V >= the leaving row in every column, so no borrow crosses a 16-bit half
         V0 = V0 - (ow & 0x00FF00FFu) + (nw & 0x00FF00FFu);
         V1 = V1 - ((ow >> 8) & 0x00FF00FFu) + ((nw >> 8) & 0x00FF00FFu);
