@@ -42,23 +42,34 @@ void note_launch(int n);
 constexpr int kStripCols = 576;                 // table columns per CTA
 constexpr int kStripSpan = 896;                 // raster columns per CTA (576 + halo, 28 per lane)
 constexpr int kStripRows = 16;                  // rows per step
-constexpr int kStripThreads = 512;              // 16 warps
-constexpr int kStripNS = 3;                     // TMA ring depth (steps in flight + 2)
+constexpr int kStripNS = 3;                     // TMA ring depth
 constexpr int kStripRowB = kStripSpan + 64;     // staged row: 16 pad + span + misalignment + tail
-constexpr int kStripVThreads = kStripSpan / 4;  // 224 threads own 4 columns each of V
-constexpr int kStripTThreads = kStripCols / 4;  // 144 threads own 4 table columns each
+constexpr int kStripVThreads = kStripSpan / 4;  // group A: 224 threads own 4 columns each of V
+constexpr int kStripTThreads = kStripCols / 4;  // group C: 144 threads own 4 table columns each
 constexpr int kStripPWords = 960;               // per-warp prefix buffer (packed_sums_row, pp() layout)
+// warp roles: A (V update) 0..6, B (window rows, 2 per warp) 7..14, C (table) 15..19;
+// warp 19 also issues the TMA row copies
+constexpr int kWarpsA = kStripVThreads / 32, kWarpsB = kStripRows / 2, kWarpsC = 5;
+constexpr int kWarpB0 = kWarpsA, kWarpC0 = kWarpsA + kWarpsB;
+constexpr int kStripThreads = 32 * (kWarpsA + kWarpsB + kWarpsC);  // 640
+constexpr int kProducerWarp = kWarpC0 + kWarpsC - 1;
 
 struct StripSmem {
   alignas(16) unsigned char stage[kStripNS][2 * kStripRows][kStripRowB];  // rows 0..15 new, 16..31 leaving
   int offs[kStripNS][2 * kStripRows];
-  uint64_t bar[kStripNS];
-  uint32_t vs[kStripRows][2 * kStripVThreads];  // V of each row of the step (packed words)
-  uint32_t tot[kStripRows][kStripTThreads];     // 4-column byte sums of each row
-  uint32_t off[kStripRows][kStripTThreads];     // their exclusive prefix across the strip
-  uint32_t lx[kStripRows];                      // left carries of the step's rows
-  uint32_t pw[kStripThreads / 32][kStripPWords];
+  uint64_t full[kStripNS];   // stage landed (TMA transaction count)
+  uint64_t freed[kStripNS];  // stage read by groups A and C (one arrival per warp)
+  uint64_t vfull[2];         // V rows of a step written (group A)
+  uint64_t vfree[2];         // V rows of a step consumed (group B)
+  uint32_t vs[2][kStripRows][2 * kStripVThreads];  // V of each row of the step (packed words), by step parity
+  uint32_t wt[2][kStripRows][kWarpsC];             // group C: per-warp totals of each row's byte sums
+  uint32_t lx[2][kStripRows];                      // left carries of the step's rows
+  uint32_t pw[kWarpsB][kStripPWords];
 };
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 // ---- pre-pass: left carry of every (row, strip) -------------------------------
 // Lx[r][s] = sum of x[r][c] for c < 576 s (u32: at most 576 * 255 * strips).
@@ -113,63 +124,30 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
   const int s = blockIdx.x;
   const int64_t c0 = (int64_t)s * kStripCols;  // first table column = first raster column of the span
   const int64_t PC = C + 1;
-  const int64_t out_r = R - w + 1;
-  const int nout = (int)(out_c - c0 < kStripCols ? out_c - c0 : kStripCols);
   const int nsteps = (int)((R + kStripRows - 1) / kStripRows);
-  const char* base = reinterpret_cast<const char*>(in);
-  const char* end_valid = base + (R - 1) * in_ld + C;
-  const int64_t c_hi = c0 + kStripSpan < C ? c0 + kStripSpan : C;
   if (tid == 0) {
-    for (int i = 0; i < kStripNS; ++i) mbar_init(&sm.bar[i], 1);
+    for (int i = 0; i < kStripNS; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.freed[i], kWarpsA + kWarpsC);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.vfull[i], kWarpsA);
+      mbar_init(&sm.vfree[i], kWarpsB);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  // producer: warp 15, lane q < 16 stages new row r0 + q, lane 16 + q the leaving row r0 + q - w
-  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-  auto issue = [&](int b, int st) {
-    const int64_t r0 = (int64_t)b * kStripRows;
-    const int q = lane & (kStripRows - 1);
-    const bool old = lane >= kStripRows;
-    const int64_t r = r0 + q - (old ? w : 0);
-    const bool has = r0 + q < R && r >= 0;
-    unsigned char* dst = sm.stage[st][lane];
-    RowSpan sp;
-    if (has) sp = row_span(base + r * in_ld, c0, c_hi, 1, end_valid, dst);
-    sm.offs[st][lane] = has ? sp.off : kNoRow;
-    warp_issue_hint(sp, has, dst, &sm.bar[st], lane, old ? drop : keep);
-  };
-  if (warp == 15)
-    for (int b = 0; b < kStripNS - 1; ++b)
-      if (b < nsteps) issue(b, b);
 
-  // phase-1 state: V words of columns 4t..4t+3 (t < 224)
-  uint32_t V0 = 0u, V1 = 0u;
-  // phase-3 state: table accumulators of columns c0 + 4t .. +3 (t < 144)
-  uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-  uint32_t xw[kStripRows];  // the 4 new bytes of every row of the step (t < 144)
-  const int64_t tc = c0 + 4 * tid;  // table column of this thread's first accumulator
-  const bool tab = tid < kStripTThreads && tc < PC;
-  if (tab) {  // table row 0: the zero border
-    const U64x4 z{0ull, 0ull, 0ull, 0ull};
-    if (tc + 4 <= PC) st256(sat + tc, z);
-    else for (int k = 0; k < 4; ++k) if (tc + k < PC) st_cs(sat + tc + k, (uint64_t)0);
-    if (cz.trow != nullptr)
-      for (int k = 0; k < 4; ++k)
-        if (tc + k < PC) { census_add(cz.trow, cz.ntr, 0); census_add(cz.tcol, cz.ntc, tc + k); }
-  }
-
-  for (int b = 0; b < nsteps; ++b) {
-    const int st = b % kStripNS;
-    const int64_t r0 = (int64_t)b * kStripRows;
-    // the stage refilled here was released by the last barrier of step b - 1
-    if (warp == 15 && b + kStripNS - 1 < nsteps) issue(b + kStripNS - 1, (b + kStripNS - 1) % kStripNS);
-    if (tid < kStripRows) sm.lx[tid] = r0 + tid < R ? lx[(r0 + tid) * nS + s] : 0u;
-    mbar_wait(&sm.bar[st], (uint32_t)((b / kStripNS) & 1));
-    // ---- phase 1: V update (224 threads) and 4-column byte sums (144 threads)
-    if (tid < kStripVThreads) {
-      const int64_t cc = c0 + 4 * tid;
-      // bytes past the raster's last column are zero (not in the staged span)
-      const uint32_t keepmask = cc + 4 <= C ? 0xFFFFFFFFu : cc >= C ? 0u : (0xFFFFFFFFu >> (8 * (4 - (int)(C - cc))));
+  if (warp < kWarpB0) {
+    // ---- group A: vertical window sums of the 896 span columns, 4 per thread
+    const int64_t cc = c0 + 4 * tid;
+    // bytes past the raster's last column are zero (not in the staged span)
+    const uint32_t keepmask = cc + 4 <= C ? 0xFFFFFFFFu : cc >= C ? 0u : (0xFFFFFFFFu >> (8 * (4 - (int)(C - cc))));
+    uint32_t V0 = 0u, V1 = 0u;
+    for (int b = 0; b < nsteps; ++b) {
+      const int st = b % kStripNS, vb = b & 1;
+      mbar_wait(&sm.full[st], (uint32_t)((b / kStripNS) & 1));
+      if (b >= 2) mbar_wait(&sm.vfree[vb], (uint32_t)(((b - 2) >> 1) & 1));
 #pragma unroll
       for (int g = 0; g < kStripRows; ++g) {
         const int on = sm.offs[st][g], oo = sm.offs[st][kStripRows + g];
@@ -179,66 +157,126 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
         // V >= the leaving row in every column, so no borrow crosses a 16-bit half
         V0 = V0 - (ow & 0x00FF00FFu) + (nw & 0x00FF00FFu);
         V1 = V1 - ((ow >> 8) & 0x00FF00FFu) + ((nw >> 8) & 0x00FF00FFu);
-        sm.vs[g][2 * tid] = V0;
-        sm.vs[g][2 * tid + 1] = V1;
-        if (tid < kStripTThreads) {
-          xw[g] = nw;
-          sm.tot[g][tid] = __dp4a(nw, 0x01010101u, 0u);
+        sm.vs[vb][g][2 * tid] = V0;
+        sm.vs[vb][g][2 * tid + 1] = V1;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.freed[st]);
+        mbar_arrive(&sm.vfull[vb]);
+      }
+    }
+  } else if (warp < kWarpC0) {
+    // ---- group B: window sums of 2 rows per warp per step from V
+    const int bw = warp - kWarpB0;
+    const int64_t out_r = R - w + 1;
+    const int nout = (int)(out_c - c0 < kStripCols ? out_c - c0 : kStripCols);
+    for (int b = 0; b < nsteps; ++b) {
+      const int vb = b & 1;
+      mbar_wait(&sm.vfull[vb], (uint32_t)((b >> 1) & 1));
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int g = 2 * bw + rr;
+        const int64_t r = (int64_t)b * kStripRows + g;
+        const int64_t i = r - (w - 1);  // the output row whose bottom row is r
+        if (r < R && i >= 0 && i < out_r && nout > 0) {
+          uint32_t Vl[14];
+#pragma unroll
+          for (int k = 0; k < 14; ++k) Vl[k] = sm.vs[vb][g][14 * lane + k];
+          packed_sums_row<28>(Vl, sm.pw[bw], i * out_ld + c0, out, nout, w, lane, cz, i);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.vfree[vb]);
     }
-    __syncthreads();
-    // ---- phase 2: warp g owns row r0 + g
-    {
-      const int g = warp;
-      const int64_t r = r0 + g;
-      // (a) exclusive prefix of the 4-column sums across the strip
-      uint32_t carry = 0u;
-#pragma unroll
-      for (int k = 0; k < (kStripTThreads + 31) / 32; ++k) {
-        const int t = 32 * k + lane;
-        const uint32_t v = t < kStripTThreads ? sm.tot[g][t] : 0u;
-        const uint32_t inc = warp_incl_scan(v, lane);
-        if (t < kStripTThreads) sm.off[g][t] = carry + inc - v;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-      }
-      // (b) the window sums whose bottom row is r: output row r - (w - 1)
-      const int64_t i = r - (w - 1);
-      if (r < R && i >= 0 && i < out_r && nout > 0) {
-        uint32_t Vl[14];
-#pragma unroll
-        for (int k = 0; k < 14; ++k) Vl[k] = sm.vs[g][14 * lane + k];
-        packed_sums_row<28>(Vl, sm.pw[warp], i * out_ld + c0, out, nout, w, lane, cz, i);
-      }
+  } else {
+    // ---- group C: the table, 4 columns per thread; warp 19 also feeds the TMA ring
+    const int ct = tid - 32 * kWarpC0, cw = warp - kWarpC0;
+    const int64_t tc = c0 + 4 * ct;  // table column of this thread's first accumulator
+    const bool tab = ct < kStripTThreads && tc < PC;
+    const int64_t cc = tc;           // its raster columns (exclusive prefix: table col c <- image cols < c)
+    const uint32_t keepmask = !(ct < kStripTThreads) ? 0u : cc + 4 <= C ? 0xFFFFFFFFu : cc >= C ? 0u
+                                  : (0xFFFFFFFFu >> (8 * (4 - (int)(C - cc))));
+    const char* base = reinterpret_cast<const char*>(in);
+    const char* end_valid = base + (R - 1) * in_ld + C;
+    const int64_t c_hi = c0 + kStripSpan < C ? c0 + kStripSpan : C;
+    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+    // lane q < 16 stages new row r0 + q, lane 16 + q the leaving row r0 + q - w
+    auto issue = [&](int b, int st) {
+      const int64_t r0 = (int64_t)b * kStripRows;
+      const int q = lane & (kStripRows - 1);
+      const bool old = lane >= kStripRows;
+      const int64_t r = r0 + q - (old ? w : 0);
+      const bool has = r0 + q < R && r >= 0;
+      unsigned char* dst = sm.stage[st][lane];
+      RowSpan sp;
+      if (has) sp = row_span(base + r * in_ld, c0, c_hi, 1, end_valid, dst);
+      sm.offs[st][lane] = has ? sp.off : kNoRow;
+      warp_issue_hint(sp, has, dst, &sm.full[st], lane, old ? drop : keep);
+    };
+    if (warp == kProducerWarp)
+      for (int b = 0; b < kStripNS - 1; ++b)
+        if (b < nsteps) issue(b, b);
+    uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+    if (tab) {  // table row 0: the zero border
+      const U64x4 z{0ull, 0ull, 0ull, 0ull};
+      if (tc + 4 <= PC) st256(sat + tc, z);
+      else for (int k = 0; k < 4; ++k) if (tc + k < PC) st_cs(sat + tc + k, (uint64_t)0);
+      if (cz.trow != nullptr)
+        for (int k = 0; k < 4; ++k)
+          if (tc + k < PC) { census_add(cz.trow, cz.ntr, 0); census_add(cz.tcol, cz.ntc, tc + k); }
     }
-    __syncthreads();
-    // ---- phase 3: table rows r0 + 1 .. r0 + 16 (144 threads x 4 columns)
-    if (tab) {
+    for (int b = 0; b < nsteps; ++b) {
+      const int st = b % kStripNS, pb = b & 1;
+      const int64_t r0 = (int64_t)b * kStripRows;
+      if (warp == kProducerWarp && b + kStripNS - 1 < nsteps) {
+        // the stage of step b + NS - 1 last held step b - 1: wait until A and C read it
+        const int sn = (b + kStripNS - 1) % kStripNS;
+        if (b >= 1) mbar_wait(&sm.freed[sn], (uint32_t)(((b - 1) / kStripNS) & 1));
+        issue(b + kStripNS - 1, sn);
+      }
+      if (ct < kStripRows) sm.lx[pb][ct] = r0 + ct < R ? lx[(r0 + ct) * nS + s] : 0u;
+      mbar_wait(&sm.full[st], (uint32_t)((b / kStripNS) & 1));
+      uint32_t xw[kStripRows], inc[kStripRows];
 #pragma unroll
       for (int g = 0; g < kStripRows; ++g) {
-        const int64_t r = r0 + g;
-        if (r >= R) break;
-        const uint32_t x = xw[g];
-        const uint32_t b0 = x & 0xFFu, b1 = (x >> 8) & 0xFFu, b2 = (x >> 16) & 0xFFu;
-        const uint64_t left = (uint64_t)sm.lx[g] + (uint64_t)sm.off[g][tid];
-        acc[0] += left;
-        acc[1] += left + b0;
-        acc[2] += left + b0 + b1;
-        acc[3] += left + b0 + b1 + b2;
-        uint64_t* dst = sat + (r + 1) * sat_ld + tc;
-        if (tc + 4 <= PC) {
-          const U64x4 v{acc[0], acc[1], acc[2], acc[3]};
-          st256(dst, v);
-        } else {
-          for (int k = 0; k < 4; ++k)
-            if (tc + k < PC) st_cs(dst + k, acc[k]);
+        const int on = sm.offs[st][g];
+        xw[g] = on == kNoRow ? 0u : row_word(sm.stage[st][g], 16 + on + (int)cc) & keepmask;
+        const uint32_t t4 = __dp4a(xw[g], 0x01010101u, 0u);
+        inc[g] = warp_incl_scan(t4, lane) - t4;  // exclusive prefix within the warp
+        if (lane == 31) sm.wt[pb][g][cw] = inc[g] + t4;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.freed[st]);
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarpsC) : "memory");  // group C only
+      if (tab) {
+#pragma unroll
+        for (int g = 0; g < kStripRows; ++g) {
+          const int64_t r = r0 + g;
+          if (r >= R) break;
+          uint32_t left32 = inc[g];
+          for (int k = 0; k < cw; ++k) left32 += sm.wt[pb][g][k];
+          const uint32_t x = xw[g];
+          const uint32_t b0 = x & 0xFFu, b1 = (x >> 8) & 0xFFu, b2 = (x >> 16) & 0xFFu;
+          const uint64_t left = (uint64_t)sm.lx[pb][g] + (uint64_t)left32;
+          acc[0] += left;
+          acc[1] += left + b0;
+          acc[2] += left + b0 + b1;
+          acc[3] += left + b0 + b1 + b2;
+          uint64_t* dst = sat + (r + 1) * sat_ld + tc;
+          if (tc + 4 <= PC) {
+            const U64x4 v{acc[0], acc[1], acc[2], acc[3]};
+            st256(dst, v);
+          } else {
+            for (int k = 0; k < 4; ++k)
+              if (tc + k < PC) st_cs(dst + k, acc[k]);
+          }
+          if (cz.trow != nullptr)
+            for (int k = 0; k < 4; ++k)
+              if (tc + k < PC) { census_add(cz.trow, cz.ntr, r + 1); census_add(cz.tcol, cz.ntc, tc + k); }
         }
-        if (cz.trow != nullptr)
-          for (int k = 0; k < 4; ++k)
-            if (tc + k < PC) { census_add(cz.trow, cz.ntr, r + 1); census_add(cz.tcol, cz.ntc, tc + k); }
       }
     }
-    __syncthreads();  // stage st, vs, tot, off and lx are reused
   }
 }
 
