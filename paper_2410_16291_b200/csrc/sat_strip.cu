@@ -36,31 +36,27 @@
 #include "ssb_stage.cuh"
 #include "ssb_packed.cuh"
 
+#ifndef SSB_STRIP_PROBE
+#define SSB_STRIP_PROBE 0  // tuning probes (wrong results): 1 no window outputs, 2 no table stores
+#endif
+
 namespace ssb {
 void note_launch(int n);
 
 constexpr int kStripCols = 576;                 // table columns per CTA
 constexpr int kStripSpan = 896;                 // raster columns per CTA (576 + halo, 28 per lane)
 constexpr int kStripRows = 16;                  // rows per step
-constexpr int kStripNS = 3;                     // TMA ring depth
-constexpr int kStripRowB = kStripSpan + 64;     // staged row: 16 pad + span + misalignment + tail
 constexpr int kStripVThreads = kStripSpan / 4;  // group A: 224 threads own 4 columns each of V
 constexpr int kStripTThreads = kStripCols / 4;  // group C: 144 threads own 4 table columns each
 constexpr int kStripPWords = 960;               // per-warp prefix buffer (packed_sums_row, pp() layout)
-// warp roles: A (V update) 0..6, B (window rows, 2 per warp) 7..14, C (table) 15..19;
-// warp 19 also issues the TMA row copies
+// warp roles: A (V update) 0..6, B (window rows, 2 per warp) 7..14, C (table) 15..19
 constexpr int kWarpsA = kStripVThreads / 32, kWarpsB = kStripRows / 2, kWarpsC = 5;
 constexpr int kWarpB0 = kWarpsA, kWarpC0 = kWarpsA + kWarpsB;
 constexpr int kStripThreads = 32 * (kWarpsA + kWarpsB + kWarpsC);  // 640
-constexpr int kProducerWarp = kWarpC0 + kWarpsC - 1;
 
 struct StripSmem {
-  alignas(16) unsigned char stage[kStripNS][2 * kStripRows][kStripRowB];  // rows 0..15 new, 16..31 leaving
-  int offs[kStripNS][2 * kStripRows];
-  uint64_t full[kStripNS];   // stage landed (TMA transaction count)
-  uint64_t freed[kStripNS];  // stage read by groups A and C (one arrival per warp)
-  uint64_t vfull[2];         // V rows of a step written (group A)
-  uint64_t vfree[2];         // V rows of a step consumed (group B)
+  uint64_t vfull[2];  // V rows of a step written (group A, one arrival per warp)
+  uint64_t vfree[2];  // V rows of a step consumed (group B)
   uint32_t vs[2][kStripRows][2 * kStripVThreads];  // V of each row of the step (packed words), by step parity
   uint32_t wt[2][kStripRows][kWarpsC];             // group C: per-warp totals of each row's byte sums
   uint32_t lx[2][kStripRows];                      // left carries of the step's rows
@@ -69,6 +65,20 @@ struct StripSmem {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 4 raster bytes [c, c + 4) of a row through L2 with a cache policy; bytes at
+// or past column C read as 0 (never loaded past the row)
+__device__ __forceinline__ uint32_t ld_word(const uint8_t* row, int64_t c, int64_t C, uint64_t pol) {
+  if (c + 4 <= C) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(row + c), "l"(pol));
+    return v;
+  }
+  uint32_t v = 0u;
+  for (int k = 0; k < 4; ++k)
+    if (c + k < C) v |= (uint32_t)__ldg(row + c + k) << (8 * k);
+  return v;
 }
 
 // ---- pre-pass: left carry of every (row, strip) -------------------------------
@@ -107,13 +117,6 @@ __global__ void __launch_bounds__(256) strip_carry_kernel(const uint8_t* __restr
   }
 }
 
-// 4 raster bytes at byte position p of a staged row (any alignment)
-__device__ __forceinline__ uint32_t row_word(const unsigned char* rowbuf, int p) {
-  const uint32_t* wd = reinterpret_cast<const uint32_t*>(rowbuf);
-  const int q = p >> 2;
-  return __funnelshift_r(wd[q], wd[q + 1], (p & 3) * 8);
-}
-
 __global__ void __launch_bounds__(kStripThreads, 1)
 sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t in_ld, uint64_t* __restrict__ sat,
                  int64_t sat_ld, uint64_t* __restrict__ out, int64_t out_ld, int64_t out_c, int w,
@@ -126,10 +129,6 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
   const int64_t PC = C + 1;
   const int nsteps = (int)((R + kStripRows - 1) / kStripRows);
   if (tid == 0) {
-    for (int i = 0; i < kStripNS; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.freed[i], kWarpsA + kWarpsC);
-    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.vfull[i], kWarpsA);
       mbar_init(&sm.vfree[i], kWarpsB);
@@ -139,32 +138,41 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
   __syncthreads();
 
   if (warp < kWarpB0) {
-    // ---- group A: vertical window sums of the 896 span columns, 4 per thread
+    // ---- group A: vertical window sums of the 896 span columns, 4 per thread.
+    // Raster words come straight from global memory (coalesced 128-byte warp
+    // loads): entering rows with an evict_last policy (they are read again w
+    // rows later, as leaving rows, from L2), leaving rows with evict_first.
+    // The next step's words are loaded while this step is computed.
     const int64_t cc = c0 + 4 * tid;
-    // bytes past the raster's last column are zero (not in the staged span)
-    const uint32_t keepmask = cc + 4 <= C ? 0xFFFFFFFFu : cc >= C ? 0u : (0xFFFFFFFFu >> (8 * (4 - (int)(C - cc))));
+    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+    uint32_t nw[kStripRows], ow[kStripRows];
+    auto load = [&](int b) {
+#pragma unroll
+      for (int g = 0; g < kStripRows; ++g) {
+        const int64_t r = (int64_t)b * kStripRows + g, ro = r - w;
+        nw[g] = r < R && cc < C ? ld_word(in + r * in_ld, cc, C, keep) : 0u;
+        ow[g] = r < R && ro >= 0 && cc < C ? ld_word(in + ro * in_ld, cc, C, drop) : 0u;
+      }
+    };
+    load(0);
     uint32_t V0 = 0u, V1 = 0u;
     for (int b = 0; b < nsteps; ++b) {
-      const int st = b % kStripNS, vb = b & 1;
-      mbar_wait(&sm.full[st], (uint32_t)((b / kStripNS) & 1));
+      const int vb = b & 1;
+      uint32_t cn[kStripRows], co[kStripRows];
+#pragma unroll
+      for (int g = 0; g < kStripRows; ++g) { cn[g] = nw[g]; co[g] = ow[g]; }
+      if (b + 1 < nsteps) load(b + 1);
       if (b >= 2) mbar_wait(&sm.vfree[vb], (uint32_t)(((b - 2) >> 1) & 1));
 #pragma unroll
       for (int g = 0; g < kStripRows; ++g) {
-        const int on = sm.offs[st][g], oo = sm.offs[st][kStripRows + g];
-        // image column c sits at byte 16 + off + c of a staged row (ssb_stage.cuh)
-        const uint32_t nw = on == kNoRow ? 0u : row_word(sm.stage[st][g], 16 + on + (int)cc) & keepmask;
-        const uint32_t ow = oo == kNoRow ? 0u : row_word(sm.stage[st][kStripRows + g], 16 + oo + (int)cc) & keepmask;
         // V >= the leaving row in every column, so no borrow crosses a 16-bit half
-        V0 = V0 - (ow & 0x00FF00FFu) + (nw & 0x00FF00FFu);
-        V1 = V1 - ((ow >> 8) & 0x00FF00FFu) + ((nw >> 8) & 0x00FF00FFu);
+        V0 = V0 - (co[g] & 0x00FF00FFu) + (cn[g] & 0x00FF00FFu);
+        V1 = V1 - ((co[g] >> 8) & 0x00FF00FFu) + ((cn[g] >> 8) & 0x00FF00FFu);
         sm.vs[vb][g][2 * tid] = V0;
         sm.vs[vb][g][2 * tid + 1] = V1;
       }
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&sm.freed[st]);
-        mbar_arrive(&sm.vfull[vb]);
-      }
+      if (lane == 0) mbar_arrive(&sm.vfull[vb]);
     }
   } else if (warp < kWarpC0) {
     // ---- group B: window sums of 2 rows per warp per step from V
@@ -179,7 +187,7 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
         const int g = 2 * bw + rr;
         const int64_t r = (int64_t)b * kStripRows + g;
         const int64_t i = r - (w - 1);  // the output row whose bottom row is r
-        if (r < R && i >= 0 && i < out_r && nout > 0) {
+        if (!(SSB_STRIP_PROBE & 1) && r < R && i >= 0 && i < out_r && nout > 0) {
           uint32_t Vl[14];
 #pragma unroll
           for (int k = 0; k < 14; ++k) Vl[k] = sm.vs[vb][g][14 * lane + k];
@@ -190,33 +198,23 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
       if (lane == 0) mbar_arrive(&sm.vfree[vb]);
     }
   } else {
-    // ---- group C: the table, 4 columns per thread; warp 19 also feeds the TMA ring
+    // ---- group C: the table, 4 columns per thread (the same raster words as
+    // group A's first 144 threads, mostly L1/L2 hits)
     const int ct = tid - 32 * kWarpC0, cw = warp - kWarpC0;
     const int64_t tc = c0 + 4 * ct;  // table column of this thread's first accumulator
     const bool tab = ct < kStripTThreads && tc < PC;
-    const int64_t cc = tc;           // its raster columns (exclusive prefix: table col c <- image cols < c)
-    const uint32_t keepmask = !(ct < kStripTThreads) ? 0u : cc + 4 <= C ? 0xFFFFFFFFu : cc >= C ? 0u
-                                  : (0xFFFFFFFFu >> (8 * (4 - (int)(C - cc))));
-    const char* base = reinterpret_cast<const char*>(in);
-    const char* end_valid = base + (R - 1) * in_ld + C;
-    const int64_t c_hi = c0 + kStripSpan < C ? c0 + kStripSpan : C;
-    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-    // lane q < 16 stages new row r0 + q, lane 16 + q the leaving row r0 + q - w
-    auto issue = [&](int b, int st) {
-      const int64_t r0 = (int64_t)b * kStripRows;
-      const int q = lane & (kStripRows - 1);
-      const bool old = lane >= kStripRows;
-      const int64_t r = r0 + q - (old ? w : 0);
-      const bool has = r0 + q < R && r >= 0;
-      unsigned char* dst = sm.stage[st][lane];
-      RowSpan sp;
-      if (has) sp = row_span(base + r * in_ld, c0, c_hi, 1, end_valid, dst);
-      sm.offs[st][lane] = has ? sp.off : kNoRow;
-      warp_issue_hint(sp, has, dst, &sm.full[st], lane, old ? drop : keep);
+    const int64_t cc = tc;           // its raster columns (table col c <- image cols < c)
+    const bool ldr = ct < kStripTThreads && cc < C;
+    const uint64_t pol = policy_evict_last();
+    uint32_t nw[kStripRows];
+    auto load = [&](int b) {
+#pragma unroll
+      for (int g = 0; g < kStripRows; ++g) {
+        const int64_t r = (int64_t)b * kStripRows + g;
+        nw[g] = ldr && r < R ? ld_word(in + r * in_ld, cc, C, pol) : 0u;
+      }
     };
-    if (warp == kProducerWarp)
-      for (int b = 0; b < kStripNS - 1; ++b)
-        if (b < nsteps) issue(b, b);
+    load(0);
     uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
     if (tab) {  // table row 0: the zero border
       const U64x4 z{0ull, 0ull, 0ull, 0ull};
@@ -227,27 +225,19 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
           if (tc + k < PC) { census_add(cz.trow, cz.ntr, 0); census_add(cz.tcol, cz.ntc, tc + k); }
     }
     for (int b = 0; b < nsteps; ++b) {
-      const int st = b % kStripNS, pb = b & 1;
+      const int pb = b & 1;
       const int64_t r0 = (int64_t)b * kStripRows;
-      if (warp == kProducerWarp && b + kStripNS - 1 < nsteps) {
-        // the stage of step b + NS - 1 last held step b - 1: wait until A and C read it
-        const int sn = (b + kStripNS - 1) % kStripNS;
-        if (b >= 1) mbar_wait(&sm.freed[sn], (uint32_t)(((b - 1) / kStripNS) & 1));
-        issue(b + kStripNS - 1, sn);
-      }
       if (ct < kStripRows) sm.lx[pb][ct] = r0 + ct < R ? lx[(r0 + ct) * nS + s] : 0u;
-      mbar_wait(&sm.full[st], (uint32_t)((b / kStripNS) & 1));
       uint32_t xw[kStripRows], inc[kStripRows];
 #pragma unroll
+      for (int g = 0; g < kStripRows; ++g) xw[g] = nw[g];
+      if (b + 1 < nsteps) load(b + 1);
+#pragma unroll
       for (int g = 0; g < kStripRows; ++g) {
-        const int on = sm.offs[st][g];
-        xw[g] = on == kNoRow ? 0u : row_word(sm.stage[st][g], 16 + on + (int)cc) & keepmask;
         const uint32_t t4 = __dp4a(xw[g], 0x01010101u, 0u);
         inc[g] = warp_incl_scan(t4, lane) - t4;  // exclusive prefix within the warp
         if (lane == 31) sm.wt[pb][g][cw] = inc[g] + t4;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.freed[st]);
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarpsC) : "memory");  // group C only
       if (tab) {
 #pragma unroll
@@ -264,7 +254,9 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
           acc[2] += left + b0 + b1;
           acc[3] += left + b0 + b1 + b2;
           uint64_t* dst = sat + (r + 1) * sat_ld + tc;
-          if (tc + 4 <= PC) {
+          if (SSB_STRIP_PROBE & 2) {
+            if (acc[0] == 0x123456789ull) st_cs(dst, acc[1]);  // keep the arithmetic alive
+          } else if (tc + 4 <= PC) {
             const U64x4 v{acc[0], acc[1], acc[2], acc[3]};
             st256(dst, v);
           } else {
@@ -280,11 +272,13 @@ sat_strip_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C, int64_t i
   }
 }
 
-bool sat_strip_supported(int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask, int64_t sat_ld) {
+bool sat_strip_supported(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
+                         int64_t sat_ld) {
   // uint8 sums, w <= 256 (16-bit V halves), rasters wide enough to give every
   // SM a strip, 8-byte aligned rows for the carry pre-pass
   return dtype == IN_U8 && mask == ST_SUM && w <= 256 && C >= (int64_t)kNumSMs * kStripCols / 2 && R >= w &&
-         (in_ld % 8) == 0 && (sat_ld % 4) == 0 && C * 255 < ((int64_t)1 << 32);
+         (in_ld % 8) == 0 && (reinterpret_cast<uintptr_t>(in) % 8) == 0 && (sat_ld % 4) == 0 &&
+         C * 255 < ((int64_t)1 << 32);
 }
 
 int64_t sat_strip_workspace_bytes(int64_t R, int64_t C) {

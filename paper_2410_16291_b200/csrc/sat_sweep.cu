@@ -519,7 +519,8 @@ bool sat_sweep_supported(int dtype, int64_t w, int mask) {
 int64_t sat_workspace_bytes(int dtype, int64_t R, int64_t C, bool sq);
 
 int64_t sat_strip_workspace_bytes(int64_t R, int64_t C);
-bool sat_strip_supported(int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask, int64_t sat_ld);
+bool sat_strip_supported(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
+                         int64_t sat_ld);
 cudaError_t launch_sat_strip(const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld, int64_t w,
                              WinOut o, void* ws, cudaStream_t st);
 
@@ -680,7 +681,7 @@ cudaError_t side_join(cudaStream_t st, const SideHandle& h) {
 cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld,
                              int64_t w, int mask, WinOut o, void* ws, cudaStream_t st, bool onepass) {
   if (!onepass && !swa_onepass_env()) {
-    if (!swa_pair_env() && sat_strip_supported(dtype, R, C, in_ld, w, mask, sat_ld))
+    if (!swa_pair_env() && sat_strip_supported(in, dtype, R, C, in_ld, w, mask, sat_ld))
       return launch_sat_strip(in, R, C, in_ld, sat, sat_ld, w, o, ws, st);
     if (!sweep_uses_fused(dtype, R, C, w)) {
       cudaError_t e = launch_sat_build(dtype, in, R, C, in_ld, sat, nullptr, sat_ld, nullptr, nullptr, ws, nullptr, st);
