@@ -518,18 +518,10 @@ bool sat_sweep_supported(int dtype, int64_t w, int mask) {
 
 int64_t sat_workspace_bytes(int dtype, int64_t R, int64_t C, bool sq);
 
-int64_t sat_strip_workspace_bytes(int64_t R, int64_t C);
-bool sat_strip_supported(const void* in, int dtype, int64_t R, int64_t C, int64_t in_ld, int64_t w, int mask,
-                         int64_t sat_ld);
-cudaError_t launch_sat_strip(const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld, int64_t w,
-                             WinOut o, void* ws, cudaStream_t st);
-
 int64_t sat_sweep_workspace_bytes(int dtype, int64_t R, int64_t C) {
   const int64_t one = make_sat_plan(dtype, R, C, false).total * 8;
   const int64_t two = sat_workspace_bytes(dtype, R, C, false);  // includes the look-back build's needs
-  const int64_t three = dtype == IN_U8 ? sat_strip_workspace_bytes(R, C) : 0;  // strip sweep carries
-  const int64_t m = one > two ? one : two;
-  return m > three ? m : three;
+  return one > two ? one : two;
 }
 
 void sat_sweep_plan_info(int dtype, int64_t R, int64_t C, int64_t w, int64_t* info) {
@@ -582,11 +574,7 @@ static bool swa_onepass_env() {
   static const bool one = env_char("SSB_SWA_PATH") == 'o';
   return one;
 }
-// SSB_SWA_PATH=pair: the concurrent build || fused pair even where the strip sweep applies (A/B)
-static bool swa_pair_env() {
-  static const bool pair = env_char("SSB_SWA_PATH") == 'p';
-  return pair;
-}
+
 
 // The fused kernel outruns the corner sweep for uint8 (w <= 256) and uint16
 // (w <= 128) rasters of at least 2^24 pixels (measured, scripts/pipe_probe.py,
@@ -681,8 +669,6 @@ cudaError_t side_join(cudaStream_t st, const SideHandle& h) {
 cudaError_t launch_sat_sweep(int dtype, const void* in, int64_t R, int64_t C, int64_t in_ld, void* sat, int64_t sat_ld,
                              int64_t w, int mask, WinOut o, void* ws, cudaStream_t st, bool onepass) {
   if (!onepass && !swa_onepass_env()) {
-    if (!swa_pair_env() && sat_strip_supported(in, dtype, R, C, in_ld, w, mask, sat_ld))
-      return launch_sat_strip(in, R, C, in_ld, sat, sat_ld, w, o, ws, st);
     if (!sweep_uses_fused(dtype, R, C, w)) {
       cudaError_t e = launch_sat_build(dtype, in, R, C, in_ld, sat, nullptr, sat_ld, nullptr, nullptr, ws, nullptr, st);
       if (e != cudaSuccess) return e;
