@@ -221,6 +221,14 @@ def fused_windows(x, kind: ElemKind, rows: int, cols: int, windows, stats, devic
     return outs
 
 
+def multi_fused_wins(kind: ElemKind, rows: int, cols: int, windows) -> bool:
+    """multi_window "auto": integer rasters of >= 2^24 pixels whose windows all
+    fit the fused kernel take concurrent fused launches instead of one table
+    (measured at C3, 30,000^2 u8, w = 25..400: 8.65 vs 10.79 ms)."""
+    return (kind is not ElemKind.F32 and rows * cols >= (1 << 24) and len(windows) > 1
+            and max(windows) <= fused_max_w())
+
+
 def fused_max_w() -> int:
     return int(_lib.load().ssb_window_fused_max_w())
 

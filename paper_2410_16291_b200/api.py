@@ -98,9 +98,12 @@ def swa(array, window: int, stat: str = "sum", method: str = "parallel", stride:
 def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str = "auto") -> list:
     """Several window sizes (api.py:58-67); stride 1.
 
-    ``"auto"``: integer rasters build the table once for the whole window set,
-    like the reference; float windows follow the same rule as ``swa`` (so
-    output i is bit-identical to ``swa(array, windows[i], stat)``).
+    ``"auto"``: large integer rasters evaluate every window without a table,
+    the launches overlapped on concurrent streams (C3: 8.7 ms vs 10.8 ms for
+    one table + one multi-window sweep; integer results are exact either
+    way); small integer rasters build the table once, like the reference;
+    float windows follow the same rule as ``swa`` (so output i is
+    bit-identical to ``swa(array, windows[i], stat)``).
     ``"table"`` forces one table set for every window; ``"fused"`` evaluates
     each window without a table."""
     img = _as_grid(array)
@@ -114,6 +117,8 @@ def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str 
         raise ValueError(f"unknown pipeline {pipeline!r}; expected auto, table, or fused")
     from .integral import _run_tables
 
+    if pipeline == "auto" and _engine.multi_fused_wins(img.elem_kind, img.rows, img.cols, windows):
+        pipeline = "fused"
     if pipeline in ("auto", "table"):
         grid = img if img.on_device else ImageGrid(img.values, img.elem_kind, _check_finite=False)
         return [r.values for r in _run_tables(grid, specs, kind, force_table=pipeline == "table")]

@@ -67,7 +67,7 @@ def test_c2_int32(sb, hashes, dev, pipe):
     assert digest(host(res["mean"], np.float64)) == hashes["C2_mean_w100"]
 
 
-@pytest.mark.parametrize("pipe", ["table", "fused"])
+@pytest.mark.parametrize("pipe", ["table", "fused", "auto"])
 def test_c3_multi_window(sb, hashes, dev, pipe):
     from paper_2410_16291_b200 import synthetic
 
