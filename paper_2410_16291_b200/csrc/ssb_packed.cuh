@@ -78,7 +78,6 @@ __device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint
       const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
       const uint2 B = *reinterpret_cast<const uint2*>(pb + 66 * qq);
       st_pair(dst + 64 * qq, (uint64_t)(B.x - A.x), (uint64_t)(B.y - A.y));
-      census_add(cz.orow, cz.nor, i, 2ull);
     }
   } else {
     const uint32_t* pb0 = P + pp(vb);
@@ -87,9 +86,9 @@ __device__ __forceinline__ void packed_sums_row(const uint32_t (&V)[E / 2], uint
     for (int qq = 0; qq < nq; ++qq) {
       const uint2 A = *reinterpret_cast<const uint2*>(pa + 66 * qq);
       st_pair(dst + 64 * qq, (uint64_t)(pb0[66 * qq] - A.x), (uint64_t)(pb1[66 * qq] - A.y));
-      census_add(cz.orow, cz.nor, i, 2ull);
     }
   }
+  census_add(cz.orow, cz.nor, i, 2ull * (unsigned long long)nq);  // this lane's pairs of row i
   __syncwarp();  // P is rewritten by the next row
 }
 

@@ -461,8 +461,8 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
           const VT sv = sub(sm.p[bw], sm.p[a]);
           if constexpr (sizeof(VT) == 4) st_cs(dst, (uint64_t)(uint32_t)sv);
           else st_cs(dst, (uint64_t)sv);
-          census_add(g.cz.orow, g.cz.nor, i);
         }
+        census_add(g.cz.orow, g.cz.nor, i, (unsigned long long)nq);  // this lane's stores of row i
       } else {
         // MASKT != 0: the stat set is a compile-time constant (no per-output tests)
         const int mk = MASKT != 0 ? MASKT : g.mask;
@@ -488,8 +488,8 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
             if (mk & ST_MEAN) st_cs(p_mean, fin_mean_int(s64, fi));
             if (mk & ST_STD) st_cs(p_std, fin_std_int(s64, q64, fi));
           }
-          census_add(g.cz.orow, g.cz.nor, i);
         }
+        census_add(g.cz.orow, g.cz.nor, i, (unsigned long long)nq);  // this lane's stores of row i
       }
       __syncwarp();
     }
