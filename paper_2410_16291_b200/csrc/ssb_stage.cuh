@@ -60,6 +60,19 @@ __device__ __forceinline__ void warp_issue(const RowSpan& sp, bool has, unsigned
   if (has && sp.b > sp.a) bulk_g2s(dst_row + 16, sp.a, (uint32_t)(sp.b - sp.a), bar);
 }
 
+// Per-lane arming: the mbarrier is initialised with one arrival per issuing
+// lane (lanes [0, nl)); each of them arms its own byte count and issues its
+// copy, so no warp-wide byte reduction or extra __syncwarp is needed (lanes
+// without a row arrive with 0 bytes).  Lanes >= nl do nothing.
+__device__ __forceinline__ void lane_issue(const RowSpan& sp, bool has, unsigned char* dst_row, uint64_t* bar, int lane,
+                                           int nl) {
+  if (lane >= nl) return;
+  const uint32_t bytes = (has && sp.b > sp.a) ? (uint32_t)(sp.b - sp.a) : 0u;
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, bytes);
+  if (bytes) bulk_g2s(dst_row + 16, sp.a, bytes, bar);
+}
+
 // warp_issue with an L2 cache policy on the bulk copies (createpolicy operand)
 __device__ __forceinline__ void warp_issue_hint(const RowSpan& sp, bool has, unsigned char* dst_row, uint64_t* bar,
                                                 int lane, uint64_t pol) {
@@ -130,6 +143,56 @@ __device__ __forceinline__ void lane_elems_packed(const unsigned char* rowbuf, i
 #pragma unroll
     for (int k = 0; k < E; ++k)
       if (c0 + k < 0 || c0 + k >= C) clear_elem<InT>(o, k);
+  }
+}
+
+// The lane's valid elements [klo, khi) of E columns starting at image column
+// c0 (columns outside [0, C) read as 0).  Computed once per sweep, so the
+// per-row extraction needs no 64-bit per-element bounds tests: interior lanes
+// (full) take no clearing at all.
+struct LaneRange {
+  int klo, khi;
+  bool full;
+};
+template <int E>
+__device__ __forceinline__ LaneRange lane_range(int64_t c0, int64_t C) {
+  LaneRange r;
+  r.klo = c0 < 0 ? (int)min64(-c0, E) : 0;
+  r.khi = (int)max64(0, min64(E, C - c0));
+  r.full = r.klo == 0 && r.khi == E;
+  return r;
+}
+
+// lane_elems_packed with a precomputed LaneRange and a shift-free path for
+// lanes whose data starts on a 16-byte boundary of the row buffer.
+template <typename InT, int E>
+__device__ __forceinline__ void lane_elems_ranged(const unsigned char* rowbuf, int off, int64_t c0, const LaneRange& lr,
+                                                  uint32_t (&o)[E * sizeof(InT) / 4]) {
+  constexpr int NO = E * (int)sizeof(InT) / 4;
+  if (off == kNoRow) {
+#pragma unroll
+    for (int k = 0; k < NO; ++k) o[k] = 0u;
+    return;
+  }
+  const int Q = 16 + off + (int)(c0 * (int64_t)sizeof(InT));
+  if ((Q & 15) == 0) {  // 16-byte aligned lane data (warp-uniform): plain vector loads
+    const uint4* p = reinterpret_cast<const uint4*>(rowbuf + Q);
+    if constexpr (NO % 4 == 0) {
+#pragma unroll
+      for (int c = 0; c < NO / 4; ++c) {
+        const uint4 v = p[c];
+        o[4 * c] = v.x; o[4 * c + 1] = v.y; o[4 * c + 2] = v.z; o[4 * c + 3] = v.w;
+      }
+    } else {
+      lane_bytes<E * (int)sizeof(InT)>(rowbuf, Q, o);
+    }
+  } else {
+    lane_bytes<E * (int)sizeof(InT)>(rowbuf, Q, o);
+  }
+  if (!lr.full) {
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (k < lr.klo || k >= lr.khi) clear_elem<InT>(o, k);
   }
 }
 

@@ -1,0 +1,2 @@
+bash scripts/gpu_ab.sh
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_fuzz.py -x -q -m gpu > gpurun_out/t_sub.log 2>&1; echo "rc=$?" >> gpurun_out/t_sub.log
