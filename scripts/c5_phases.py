@@ -60,7 +60,30 @@ def t(fn, n=8):
     return round(a.elapsed_time(b) / n, 3)
 
 
+def concurrent(n=8):
+    """build on this stream, windows on a side stream, both forked from one event:
+    (build end, windows end) relative to the fork, ms"""
+    side = torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+    b_end, w_end = [], []
+    for i in range(3 + n):
+        e0, e1, f1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(cur)
+        side.wait_event(e0)
+        build()
+        e1.record(cur)
+        _lib.check(lib.ssb_window_fused(x.data_ptr(), 0, R, C, C, W, _lib.SUM, out.data_ptr(), None, None, OC, None, 0,
+                                        side.cuda_stream))
+        f1.record(side)
+        cur.wait_event(f1)
+        torch.cuda.synchronize()
+        if i >= 3:
+            b_end.append(e0.elapsed_time(e1))
+            w_end.append(e0.elapsed_time(f1))
+    return round(sum(b_end) / n, 3), round(sum(w_end) / n, 3)
+
+
 prep()
 res = {"lib": os.environ.get("SSB_LIB", "product"), "prepare": t(prep), "scan": t(fin), "build": t(build),
-       "windows": t(windows), "step": t(step, 10)}
+       "windows": t(windows), "step": t(step, 10), "concurrent_build_windows_end": concurrent()}
 print(json.dumps(res), flush=True)
