@@ -47,9 +47,6 @@
 #ifndef SSB_SCAN_RB
 #define SSB_SCAN_RB 0  // rows per TMA stage in the scan (0: 8 for 1-byte, 4 for wider pixels)
 #endif
-#ifndef SSB_SCAN_IL
-#define SSB_SCAN_IL 0  // 1: lane-interleaved column groups (contiguous 1 KB warp stores; measured slower, DESIGN 9)
-#endif
 #ifndef SSB_SCAN_MINB_SQ
 #define SSB_SCAN_MINB_SQ 2
 #endif
@@ -487,223 +484,6 @@ sat_scan_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
 }
 
 // ---------------------------------------------------------------------------
-// phase 3, integer kinds: lane-interleaved columns.  Same tiles, staging and
-// arithmetic as sat_scan_kernel, but lane l owns E/4 groups of 4 consecutive
-// table columns at j0 + 128 g + 4 l, so each 256-bit store instruction of the
-// warp writes 1 KB of contiguous table row instead of 32 pieces 128 B apart.
-// Measured on this B200 (scripts/probes/wr_probe2.cu, pure table-tile
-// writes): 6.85 vs 6.38 TB/s at 512-row segments, 7.13 vs 6.58 TB/s at 128.
-// The strip-local row prefix becomes one warp scan per group (two 16-bit
-// groups share one 32-bit scan for uint8 sums: a 128-column group prefix is
-// at most 32,640) plus the running totals of the groups to the left.
-// Integer tables are exact modulo 2^64, so the different association gives
-// the same bits as sat_scan_kernel.
-template <typename InT>
-__device__ __forceinline__ void group_words(const unsigned char* rowbuf, int off, int64_t c, int64_t C,
-                                            uint32_t (&o)[sizeof(InT)]) {
-  constexpr int NW = (int)sizeof(InT);  // 4 elements = NW words
-  if (off == kNoRow) {
-#pragma unroll
-    for (int k = 0; k < NW; ++k) o[k] = 0u;
-    return;
-  }
-  const int Q = 16 + off + (int)(c * (int64_t)sizeof(InT));  // byte of element c; Q & 3 is warp-uniform
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(rowbuf + (Q & ~3));
-  const int sb = (Q & 3) * 8;
-  uint32_t w[NW + 1];
-#pragma unroll
-  for (int k = 0; k <= NW; ++k) w[k] = wp[k];
-#pragma unroll
-  for (int k = 0; k < NW; ++k) o[k] = __funnelshift_r(w[k], w[k + 1], sb);
-  if (c < 0 || c + 4 > C) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (c + k < 0 || c + k >= C) clear_elem<InT>(o, k);
-  }
-}
-
-template <typename InT, bool SQ>
-__global__ void __launch_bounds__(32 * kScanWarps, SQ ? SSB_SCAN_MINB_SQ : SSB_SCAN_MINB)
-sat_scan_il_kernel(const InT* __restrict__ in, int64_t R, int64_t C, int64_t in_ld,
-                   typename Elem<InT>::Acc* __restrict__ sat, typename Elem<InT>::Acc* __restrict__ sat_sq,
-                   int64_t sat_ld, const typename Elem<InT>::Acc* __restrict__ rl,
-                   const typename Elem<InT>::Acc* __restrict__ rl_sq, const typename Elem<InT>::Acc* __restrict__ top,
-                   const typename Elem<InT>::Acc* __restrict__ top_sq, int64_t SR, int nJ, int nK, Census cz) {
-  using Tr = Elem<InT>;
-  using Loc = typename Tr::Loc;
-  using LocSq = typename Tr::LocSq;
-  using Acc = typename Tr::Acc;
-  using G = Geo<InT>;
-  using WS = WarpStage<InT, SSB_SCAN_RB, SSB_SCAN_STAGES>;
-  constexpr int E = G::E, NG = E / 4, RB = WS::RBW, NSTG = WS::NSTG, ES = G::ES;
-  static_assert(!Tr::kFloat && E % 4 == 0, "integer kinds, whole groups of 4");
-  constexpr bool kPack16 = ES == 1 && NG % 2 == 0;  // uint8 sums: two 16-bit group prefixes per scan
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  WS* stages = reinterpret_cast<WS*>(smem_raw);
-  const int lane = threadIdx.x & 31;
-  WS& ws = stages[threadIdx.x >> 5];
-  int J, K;
-  warp_tile<kScanWarps>(nJ, nK, J, K);
-  if (K < 0) return;
-  const int64_t PR = R + 1, PC = C + 1;
-  const int64_t j0 = (int64_t)J * G::TW, k0 = (int64_t)K * SR;
-  const int64_t k1 = min(k0 + SR, PR);
-  const int nblk = (int)((k1 - k0 + RB - 1) / RB);
-  const int64_t cl = j0 + 4 * lane;  // table column of the lane's first element in group 0
-  warp_stage_init(ws, lane);
-#pragma unroll
-  for (int pb = 0; pb < NSTG - 1; ++pb) {
-    if (pb < nblk) {
-      const int64_t rp = k0 + (int64_t)pb * RB;
-      stage_issue<InT, RB>(ws.buf[pb], ws.offs[pb], &ws.bar[pb], in, R, C, in_ld, rp, (int)min64(RB, k1 - rp), j0,
-                           lane);
-    }
-  }
-  Acc acc[E], accq[E];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t col = cl + 128 * g + i;
-      acc[4 * g + i] = col < PC ? top[(int64_t)K * PC + col] : Acc(0);
-      if constexpr (SQ) accq[4 * g + i] = col < PC ? top_sq[(int64_t)K * PC + col] : Acc(0);
-    }
-  }
-  const bool writes_plain = sat != nullptr;
-  auto store_group = [&](Acc* dst_row, const Acc* v, int g) {
-    const int64_t col = cl + 128 * g;
-    Acc* dst = dst_row + col;
-    if (col + 4 <= PC) {
-      U64x4 q;
-      memcpy(&q, v, 32);
-      st256(dst, q);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (col + i < PC) st_cs(dst + i, v[i]);
-    }
-  };
-
-  for (int b = 0; b < nblk; ++b) {
-    const int s = b % NSTG;
-    const int64_t r0 = k0 + (int64_t)b * RB;
-    const int nr = (int)min64(RB, k1 - r0);
-    if (b + NSTG - 1 < nblk) {
-      const int sn = (b + NSTG - 1) % NSTG;
-      const int64_t rn = r0 + (int64_t)(NSTG - 1) * RB;
-      stage_issue<InT, RB>(ws.buf[sn], ws.offs[sn], &ws.bar[sn], in, R, C, in_ld, rn, (int)min64(RB, k1 - rn), j0,
-                           lane);
-    }
-    Acc rlv = Acc(0), rlqv = Acc(0);
-    if (lane < nr) {
-      rlv = rl[(r0 + lane) * nJ + J];
-      if constexpr (SQ) rlqv = rl_sq[(r0 + lane) * nJ + J];
-    }
-    mbar_wait(&ws.bar[s], (uint32_t)((b / NSTG) & 1));
-    for (int r = 0; r < nr; ++r) {
-      const int64_t row = r0 + r;
-      const unsigned char* rowbuf = ws.buf[s] + r * G::ROWB;
-      const int off = ws.offs[s][r];
-      uint32_t o[NG][ES];
-#pragma unroll
-      for (int g = 0; g < NG; ++g) group_words<InT>(rowbuf, off, cl - 1 + 128 * g, C, o[g]);
-      {
-        Loc t[NG], ex[NG], tot[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          if constexpr (ES == 1) t[g] = __dp4a(o[g][0], 0x01010101u, 0u);
-          else {
-            t[g] = Loc(0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) t[g] = add(t[g], conv<Loc>(elem<InT>(o[g], i)));
-          }
-        }
-        if constexpr (kPack16) {
-#pragma unroll
-          for (int g = 0; g < NG; g += 2) {
-            const uint32_t p = t[g] | (t[g + 1] << 16);
-            const uint32_t inc = warp_incl_scan(p, lane);
-            const uint32_t exc = inc - p;
-            const uint32_t all = __shfl_sync(0xffffffffu, inc, 31);
-            ex[g] = exc & 0xFFFFu; ex[g + 1] = exc >> 16;
-            tot[g] = all & 0xFFFFu; tot[g + 1] = all >> 16;
-          }
-        } else {
-#pragma unroll
-          for (int g = 0; g < NG; ++g) {
-            const Loc inc = warp_incl_scan(t[g], lane);
-            ex[g] = sub(inc, t[g]);
-            tot[g] = __shfl_sync(0xffffffffu, inc, 31);
-          }
-        }
-        const Acc left = __shfl_sync(0xffffffffu, rlv, r);
-        Loc gc = Loc(0);  // columns of the strip in groups to the left
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          Loc run = add(gc, ex[g]);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            run = add(run, conv<Loc>(elem<InT>(o[g], i)));
-            acc[4 * g + i] = add(acc[4 * g + i], add(left, (Acc)run));
-          }
-          gc = add(gc, tot[g]);
-        }
-        if (writes_plain) {
-#pragma unroll
-          for (int g = 0; g < NG; ++g) store_group(sat + row * sat_ld, &acc[4 * g], g);
-        }
-      }
-      if constexpr (SQ) {
-        LocSq t[NG], ex[NG], tot[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          if constexpr (ES == 1) t[g] = __dp4a(o[g][0], o[g][0], 0u);
-          else {
-            t[g] = LocSq(0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) t[g] = add(t[g], convsq<LocSq>(elem<InT>(o[g], i)));
-          }
-        }
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          const LocSq inc = warp_incl_scan(t[g], lane);
-          ex[g] = sub(inc, t[g]);
-          tot[g] = __shfl_sync(0xffffffffu, inc, 31);
-        }
-        const Acc left = __shfl_sync(0xffffffffu, rlqv, r);
-        LocSq gc = LocSq(0);
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          LocSq run = add(gc, ex[g]);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            run = add(run, convsq<LocSq>(elem<InT>(o[g], i)));
-            accq[4 * g + i] = add(accq[4 * g + i], add(left, (Acc)run));
-          }
-          gc = add(gc, tot[g]);
-        }
-#pragma unroll
-        for (int g = 0; g < NG; ++g) store_group(sat_sq + row * sat_ld, &accq[4 * g], g);
-      }
-      if (cz.trow != nullptr) {  // census: table positions (row, col) this lane stored
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int64_t col = cl + 128 * g + i;
-            if (col < PC) {
-              census_add(cz.trow, cz.ntr, row);
-              census_add(cz.tcol, cz.ntc, col);
-            }
-          }
-        }
-      }
-    }
-    __syncwarp();  // stage s fully read before it is refilled
-  }
-}
-
-// ---------------------------------------------------------------------------
 // host-side launch (SatPlan / make_sat_plan: sat_plan.cuh)
 
 template <typename InT, bool SQ, int RBR, int WPC>
@@ -785,9 +565,6 @@ cudaError_t launch_sat_finish_t(const void* in, int64_t R, int64_t C, int64_t in
   const int tb = (int)(((int64_t)p.nJ * p.nK + kScanWarps - 1) / kScanWarps);
   const int smem = (int)(sizeof(WarpStage<InT, SSB_SCAN_RB, SSB_SCAN_STAGES>) * kScanWarps);
   auto kfn = sat_scan_kernel<InT, SQ>;
-#if SSB_SCAN_IL
-  if constexpr (!Elem<InT>::kFloat) kfn = sat_scan_il_kernel<InT, SQ>;  // integer kinds: lane-interleaved stores
-#endif
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   kfn<<<tb, 32 * kScanWarps, smem, st>>>(reinterpret_cast<const InT*>(in), R, C, in_ld,
