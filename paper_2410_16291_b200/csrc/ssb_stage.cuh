@@ -129,11 +129,12 @@ __device__ __forceinline__ void clear_elem(uint32_t* o, int k) {
 
 // Lane's E elements starting at image column c0 of a staged row (0 outside [0, C)
 // and for rows without data).
-template <typename InT, int E>
+// MAYBE_EMPTY = false: the caller guarantees the row has data (no select of zeros).
+template <typename InT, int E, bool MAYBE_EMPTY = true>
 __device__ __forceinline__ void lane_elems_packed(const unsigned char* rowbuf, int off, int64_t c0, int64_t C,
                                                   uint32_t (&o)[E * sizeof(InT) / 4]) {
   constexpr int NO = E * (int)sizeof(InT) / 4;
-  if (off == kNoRow) {
+  if (MAYBE_EMPTY && off == kNoRow) {
 #pragma unroll
     for (int k = 0; k < NO; ++k) o[k] = 0u;
     return;
@@ -165,11 +166,11 @@ __device__ __forceinline__ LaneRange lane_range(int64_t c0, int64_t C) {
 
 // lane_elems_packed with a precomputed LaneRange and a shift-free path for
 // lanes whose data starts on a 16-byte boundary of the row buffer.
-template <typename InT, int E>
+template <typename InT, int E, bool MAYBE_EMPTY = true>
 __device__ __forceinline__ void lane_elems_ranged(const unsigned char* rowbuf, int off, int64_t c0, const LaneRange& lr,
                                                   uint32_t (&o)[E * sizeof(InT) / 4]) {
   constexpr int NO = E * (int)sizeof(InT) / 4;
-  if (off == kNoRow) {
+  if (MAYBE_EMPTY && off == kNoRow) {
 #pragma unroll
     for (int k = 0; k < NO; ++k) o[k] = 0u;
     return;

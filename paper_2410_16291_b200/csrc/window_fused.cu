@@ -338,12 +338,14 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
   for (int k = 0; k < E; ++k) Vq[k] = VQ(0);
   bool nf = false;
   const LaneRange lr = lane_range<E>(c0, g.C);
+  // every row read below has data (new rows < R; leaving rows only from the
+  // segment's w-th row on), so no empty-row selects.
   // 4-byte pixels: bounds from the precomputed range, shift-free aligned loads
   // (C4 2.91 -> 2.75 ms, C2 0.61 -> 0.56 ms); uint8 keeps the per-row test
   // (measured 0.1 ms slower at C5 with the range)
   auto row_elems = [&](const unsigned char* rowbuf, int off, uint32_t (&x)[NW]) {
-    if constexpr (ES == 4) lane_elems_ranged<InT, E>(rowbuf, off, c0, lr, x);
-    else lane_elems_packed<InT, E>(rowbuf, off, c0, g.C, x);
+    if constexpr (ES == 4) lane_elems_ranged<InT, E, false>(rowbuf, off, c0, lr, x);
+    else lane_elems_packed<InT, E, false>(rowbuf, off, c0, g.C, x);
   };
   const int ubase = lane * E + 1;                        // first P index this lane writes
   const int addr_a = lane;                               // word of P[lane]
@@ -358,8 +360,8 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
     for (int q = 0; q < RB; ++q) {
       const int64_t r = rb + q;
       if (r >= r_end) break;
-      {
-        uint32_t oo[NW];  // row r-w (zeros until r >= r_beg + w) leaves the window first
+      if (r >= r_beg + w) {  // row r-w leaves the window first (staged from the segment's w-th row on)
+        uint32_t oo[NW];
         row_elems(sm.stage[s][RB + q], sm.offs[s][RB + q], oo);
         if constexpr (PACK) {
           // V[2i] holds columns 4i, 4i+2 and V[2i+1] columns 4i+1, 4i+3 (16-bit halves;
