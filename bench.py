@@ -260,6 +260,45 @@ def cpu_baseline(args) -> dict:
                               "build_s": seq.get("build_s"), "query_s": seq.get("query_s")}}
 
 
+# ----------------------------------------------------------------------------- C1-C4 CPU reference samples
+# per config, the reference itself on the host cores -- C1 and C2
+# whole (C2 as its uint16 cast, SUM and MEAN as the separate calls the
+# reference makes), C3's multi_window (single-threaded in the reference,
+# integral.py:209) and C4's MEAN and STD on bounded row bands, credited with
+# the band's share of the image's output rows.
+CPU_SAMPLES = {
+    "C1": (None, 50, ("sum",), "parallel"),
+    "C2": (None, 100, ("sum", "mean"), "parallel"),
+    "C3": (3000, None, None, "multi_window"),
+    "C4": (4000, 64, ("mean", "std"), "parallel"),
+}
+
+
+def cpu_config_sample(ref, name: str, host: np.ndarray) -> dict:
+    rows_in, w, stats, method = CPU_SAMPLES[name]
+    sb = ref.mod
+    x = host if rows_in is None else host[:rows_in]
+    if name == "C2":
+        x = x.astype(np.uint16)  # the reference has no int32 kind; counts fit uint16
+    t0 = time.perf_counter()
+    if method == "multi_window":
+        ws_ = [25, 50, 100, 200, 400]
+        sb.multi_window(x, ws_, "sum")
+        out_rows, full_rows = x.shape[0] - 400 + 1, host.shape[0] - 400 + 1
+        parts = None
+    else:
+        img = sb.ImageGrid(x)
+        parts = {}
+        for st in stats:
+            r = sb.bench.run_timed(method, img, sb.WindowSpec(w), sb.StatKind.parse(st), threads=0)
+            parts[st] = r.total_s
+        out_rows, full_rows = x.shape[0] - w + 1, host.shape[0] - w + 1
+    s = time.perf_counter() - t0
+    px = out_rows / full_rows * host.shape[0] * host.shape[1]
+    return {"s": s, "gpx_s": px / s / 1e9, "sample_rows": int(x.shape[0]), "calls_s": parts,
+            "method": method, "kind": ref.kind}
+
+
 # ----------------------------------------------------------------------------- C1-C4 through the public API
 def run_configs(args, dev, pk) -> dict:
     """BASELINE configs C1-C4, device-resident, through the public API (auto
@@ -296,11 +335,18 @@ def run_configs(args, dev, pk) -> dict:
         ("C4", "20000x24000 f32 lognormal, mean + std w=64 (fp64)", synthetic.c4,
          lambda x: sb.swa_stats(x, 64, ("mean", "std")), lambda r, c: r * c * 4 + 2 * (r - 63) * (c - 63) * 8),
     ]
+    ref = Reference() if not args.no_cpu else None
     for name, desc, gen, call, floor in cases:
         try:
             host = gen()
             x = torch.from_numpy(host).to(dev)
             r, c = host.shape
+            cpu = None
+            if ref is not None and ref.mod is not None:
+                try:
+                    cpu = cpu_config_sample(ref, name, host)
+                except Exception as exc:  # pragma: no cover - reporting only
+                    cpu = {"error": repr(exc)}
             del host
             steps = 20 if name == "C1" else max(3, args.steps // 2)
             ms, launches = timed(lambda: call(x), steps)
@@ -309,6 +355,10 @@ def run_configs(args, dev, pk) -> dict:
                          "floor_bytes": fb, "floor_frac": fb / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
                          "launches_per_call": launches,
                          "floor": "input read once + every output written once (the fused-pipeline floor, SURVEY 8d)"}
+            if cpu is not None:
+                res[name]["cpu_reference"] = cpu
+                if "gpx_s" in cpu:
+                    res[name]["vs_cpu_reference"] = res[name]["gpx_s"] / cpu["gpx_s"]
             del x
             sb.release_scratch()
         except Exception as exc:  # pragma: no cover - reporting only
