@@ -141,6 +141,46 @@ def test_std_examples(sb):
             np.testing.assert_array_equal(sb.swa(arr, w, "std", pipeline=pipe), np.zeros((12 - w + 1,) * 2))
 
 
+def _window_mean(x: np.ndarray, w: int) -> np.ndarray:
+    t = np.zeros((x.shape[0] + 1, x.shape[1] + 1))
+    t[1:, 1:] = x.cumsum(0).cumsum(1)
+    return (t[w:, w:] - t[:-w, w:] - t[w:, :-w] + t[:-w, :-w]) / (w * w)
+
+
+def test_float_std_edges(sb):
+    """Float std's finalisation (the reference's mean = s/n, var = q/n - mean^2
+    with correctly rounded divisions; sqrt from the rsqrt estimate of
+    var + 2^-1000 and one Newton step): constant windows of exactly summable
+    values give exactly 0 (not NaN, not a residue), as the reference does;
+    every other case -- the smallest / largest float32 magnitudes, constant
+    windows whose reference sums carry rounding noise, and windows whose
+    one-pass variance cancels -- agrees with the reference within the rtol
+    contract measured against the size of the terms, sqrt(mean(x^2)), plus
+    the table arithmetic's own noise floor: the reference's one-pass formula
+    over running sums (integral.py:141-163, stats.py:70-74) is accurate only
+    to that scale, so a result at noise level is compared at noise level."""
+    rng = np.random.default_rng(77)
+    cases = [np.full((40, 70), v, dtype=np.float32) for v in (0.0, 1.0, 3.0e-38, 1.4e-45, 3.0e38 / 64, 1234.5678)]
+    cases += [(1000.0 + rng.random((60, 90)) * 0.1).astype(np.float32),   # var / E[x^2] ~ 1e-8
+              (rng.random((60, 90)) * 1e-30).astype(np.float32),
+              (10.0 ** rng.uniform(-30, 30, (60, 90))).astype(np.float32)]
+    for k, arr in enumerate(cases):
+        # the table pipelines (the reference's and ours) difference running sums
+        # of squares that reach sum(x^2): their var carries an absolute
+        # rounding noise of ~eps * sum(x^2), so std agrees to sqrt of that
+        noise = 8.0 * np.sqrt(np.finfo(np.float64).eps * (arr.astype(np.float64) ** 2).sum())
+        for w in (1, 4, 9):
+            ref = O.swa(arr, w, "std")
+            scale = np.sqrt(np.maximum(_window_mean(arr.astype(np.float64) ** 2, w), 0.0))  # cumsum noise can dip < 0
+            for pipe in PIPES:
+                got = sb.swa(arr, w, "std", pipeline=pipe)
+                assert np.isfinite(got).all() and (got >= 0).all(), (k, w, pipe)
+                bad = np.abs(got - ref) > 1e-6 * scale + noise
+                assert not bad.any(), (k, w, pipe, np.argwhere(bad)[:3].tolist(), got[bad][:3], ref[bad][:3], noise)
+                if k < 2:  # 0.0 and 1.0: every window sum is exact -> std exactly 0
+                    assert not got.any(), (k, w, pipe)
+
+
 def test_multi_window(sb, golden):
     v = golden["mw_in"]
     for stat in ("sum", "mean", "std"):
