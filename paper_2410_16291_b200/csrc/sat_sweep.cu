@@ -11,9 +11,9 @@
 //   * default (launch_sat_sweep, bottom of the file): the reduce-then-scan
 //     build (sat_build.cu) on the caller's stream and, concurrently on a
 //     forked side stream, the fused window kernel (window_fused.cu) over the
-//     raster; the fastest on B200 (C5 19.9 ms);
+//     raster; the fastest on B200 (C5 19.8 ms);
 //   * one-pass kernel (sat_sweep_kernel): the warp that writes a table row
-//     also emits the windows whose bottom corner row it is (C5 22.9 ms,
+//     also emits the windows whose bottom corner row it is (C5 20.1 ms,
 //     latency-bound).
 //
 // One-pass kernel.  Phase 3 of the reduce-then-scan build gives every warp a
@@ -568,7 +568,7 @@ cudaError_t launch_window_eval(const void* sat, const void* sat_sq, bool is_floa
 // raster instead of reading the table back.  The two are independent, so the
 // windows run on a side stream forked from and joined back into the caller's
 // stream: measured at C5 (B200) 19.8 ms concurrent vs 21.0 ms back to back,
-// 23.0 ms for the one-pass kernel above and 24.7 ms for build + corner sweep.
+// 20.1 ms for the one-pass kernel above and 25.1 ms for build + corner sweep.
 // ssb_sat_build_swa_onepass (or SSB_SWA_PATH=onepass) runs the one-pass kernel.
 static bool swa_onepass_env() {
   static const bool one = env_char("SSB_SWA_PATH") == 'o';

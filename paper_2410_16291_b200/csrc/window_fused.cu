@@ -341,7 +341,7 @@ fused_strip_kernel(const InT* __restrict__ in, FusedGeom g, WinOut o, FinalizeIn
   // every row read below has data (new rows < R; leaving rows only from the
   // segment's w-th row on), so no empty-row selects.
   // 4-byte pixels: bounds from the precomputed range, shift-free aligned loads
-  // (C4 2.91 -> 2.75 ms, C2 0.61 -> 0.56 ms); uint8 keeps the per-row test
+  // (C4 2.91 -> 2.75 ms, C2 0.61 -> 0.56 ms at the time); uint8 keeps the per-row test
   // (measured 0.1 ms slower at C5 with the range)
   auto row_elems = [&](const unsigned char* rowbuf, int off, uint32_t (&x)[NW]) {
     if constexpr (ES == 4) lane_elems_ranged<InT, E, false>(rowbuf, off, c0, lr, x);
