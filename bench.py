@@ -30,6 +30,7 @@ ranks when WORLD_SIZE is not set.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import socket
@@ -617,6 +618,26 @@ def main() -> None:
                 times.append(time.perf_counter() - t0)
             te = statistics.median(times)
             h2d, d2h = nr * COLS, n_out * OUT_C * 8
+            wire = {}
+            if n_out > 0:
+                # what actually crossed PCIe: ssb_swa_host sends the sums as uint32 when they provably
+                # fit (w^2 * 255 < 2^32) and widens them into the uint64 result on the host
+                c_h2d, c_d2h = ctypes.c_int64(), ctypes.c_int64()
+                lib.ssb_host_last_copy_bytes(ctypes.byref(c_h2d), ctypes.byref(c_d2h))
+                h2d, d2h = int(c_h2d.value), int(c_d2h.value)
+                wire["sum_bits"] = 32 if d2h < n_out * OUT_C * 8 else 64
+                if wire["sum_bits"] == 32 and world == 1:
+                    # the same call with the straight 64-bit result copy, for the record
+                    lib.ssb_host_wire(64)
+                    try:
+                        e2e_step()
+                        t0 = time.perf_counter()
+                        e2e_step()
+                        t64 = time.perf_counter() - t0
+                    finally:
+                        lib.ssb_host_wire(0)
+                    wire["wire64"] = {"value": px / t64 / 1e9, "s_per_step": t64,
+                                      "d2h_bytes_per_step": n_out * OUT_C * 8}
             if world > 1:
                 import torch.distributed as dist
 
@@ -627,10 +648,12 @@ def main() -> None:
                 te, h2d, d2h = float(mx.item()), int(agg[1].item()), int(agg[2].item())
             result["e2e"] = {"value": px / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                              "d2h_bytes_per_step": d2h, "s_per_step": te, "steps_s": times,
-                             "d2h_gbs": d2h / te / 1e9,
+                             "d2h_gbs": d2h / te / 1e9, "wire": wire,
+                             "host_result_bytes_per_step": n_out * OUT_C * 8,
                              "api": "paper_2410_16291_b200.swa(pinned numpy, 256, 'sum', pipeline='table', out=pinned,"
-                                    " devices=[this GPU]) -> ssb_swa_host (banded H2D, table + windows, D2H); per "
-                                    "rank on its band + halo; median step, max over ranks"}
+                                    " devices=[this GPU]) -> ssb_swa_host (banded H2D, table + windows, D2H of the sums as "
+                                    "uint32 when w^2*255 < 2^32, zero-extended into the pinned uint64 result by the "
+                                    "library's host threads); per rank on its band + halo; median step, max over ranks"}
             del host_in, host_out, hin, hout
         except Exception as exc:  # pragma: no cover
             result["e2e"] = {"error": repr(exc)}

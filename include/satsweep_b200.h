@@ -181,8 +181,9 @@ int ssb_window_sum_at(const void* sat, int is_float_table, int64_t rows, int64_t
 /* End-to-end with HOST buffers: input rows x cols at pitch in_ld (elements),
  * outputs at pitch out_ld.  Streams output-row bands through the device
  * (each band builds its own local table; offsets cancel) with
- * copies overlapped on two streams.  Pinned host buffers give full PCIe
- * bandwidth; pageable ones work but are slower.  `band_rows` = output rows per
+ * copies overlapped on their own streams.  Pinned host buffers give full PCIe
+ * bandwidth; pageable ones work but are slower.  SUM results that provably
+ * fit 32 bits cross PCIe as uint32 (see ssb_host_wire).  `band_rows` = output rows per
  * band (0 = automatic). */
 int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, int64_t in_ld, int64_t w,
                  int64_t stride, int stat_mask, void* out_sum_host, double* out_mean_host, double* out_std_host,
@@ -262,8 +263,29 @@ int ssb_census_enable(unsigned long long* table_rows, int64_t n_table_rows, unsi
 int ssb_census_disable(void);
 
 /* Return the band buffers ssb_swa_host keeps reserved between calls (its
- * private pool on every device) to the device. */
+ * private pool on every device) to the device, and free its pinned staging
+ * rings. */
 int ssb_host_release(void);
+
+/* Wire format of ssb_swa_host's SUM results (api.py:28-55 returns uint64 on
+ * the host; the device->host copy of the results is the end-to-end critical
+ * path).  0 (default): when every sum provably fits 32 bits (unsigned pixels,
+ * w^2 * max pixel < 2^32) the device narrows the sums to uint32 before the
+ * copy and the library's host threads zero-extend each landed band into the
+ * caller's uint64 array -- half the PCIe bytes, the same values; every other
+ * case copies 64-bit results straight into the caller's array.  64: always
+ * the straight copy.  Returns the previous setting; other values only query. */
+int ssb_host_wire(int bits);
+
+/* Host threads each ssb_swa_host call uses to widen narrow-wire results
+ * (0 = automatic: the process's share of the cores minus two; n > 0 fixes it,
+ * e.g. cores / devices when one process drives several GPUs at once).  Returns
+ * the previous setting; negative values only query. */
+int ssb_host_threads(int n);
+
+/* Bytes the process's latest ssb_swa_host call copied host->device and
+ * device->host (what crossed PCIe, after the wire format above). */
+void ssb_host_last_copy_bytes(int64_t* h2d_bytes, int64_t* d2h_bytes);
 
 /* Count of kernel launches the library issued since load (diagnostics). */
 int64_t ssb_launch_count(void);

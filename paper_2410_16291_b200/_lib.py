@@ -71,6 +71,9 @@ _SIGS = {
     "ssb_census_enable": (_int, [_vp, _i64, _vp, _i64, _vp, _i64]),
     "ssb_census_disable": (_int, []),
     "ssb_host_release": (_int, []),
+    "ssb_host_wire": (_int, [_int]),
+    "ssb_host_threads": (_int, [_int]),
+    "ssb_host_last_copy_bytes": (None, [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "ssb_file_to_device": (_int, [ctypes.c_char_p, _i64, _i64, _vp, _int, _vp]),
     "ssb_device_to_file": (_int, [ctypes.c_char_p, _i64, _vp, _i64, _int, _vp]),
     "ssb_f32_nonfinite": (_int, [_vp, _i64, _vp, _vp]),

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsatsweep_b200.so"
-SOURCES = ["sat_build.cu", "sat_onepass.cu", "sat_sweep.cu", "window_eval.cu", "window_fused.cu", "capi.cu", "io.cu", "shard.cu", "selftest.cu"]
+SOURCES = ["sat_build.cu", "sat_onepass.cu", "sat_sweep.cu", "window_eval.cu", "window_fused.cu", "capi.cu", "io.cu", "shard.cu", "selftest.cu", "host_widen.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 

@@ -6,6 +6,9 @@
 //   allocation failure      -> SSB_ENOMEM  (ResourceLimitError, integral.py:76-83)
 //   non-finite F32 pixels   -> SSB_ENONFINITE (GridValidationError, grid.py:82-83)
 #include <atomic>
+#include <chrono>
+#include <memory>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +19,10 @@
 
 #include "ssb_common.cuh"
 #include "../../include/satsweep_b200.h"
+
+namespace ssb {
+void widen_u32_to_u64(const uint32_t* src, uint64_t* dst, size_t n);  // host_widen.cpp
+}
 
 #ifndef SSB_ENONFINITE
 #define SSB_ENONFINITE 5
@@ -373,6 +380,129 @@ cudaError_t host_pool(int device, cudaMemPool_t* out) {
   *out = pools[device];
   return cudaSuccess;
 }
+
+// ---- narrow wire format of ssb_swa_host (uint32 sums over PCIe, widened on the host) ----
+std::atomic<int> g_host_threads{0};  // widening threads per call (0: automatic)
+std::atomic<int> g_host_wire{0};  // 0: automatic (32 bits when every sum provably fits), 64: always full width
+std::atomic<int64_t> t_host_h2d{0}, t_host_d2h{0};  // bytes copied by the process's latest ssb_swa_host call
+
+// pinned staging ring, one per device, kept between calls (pinning ~2 GB takes
+// longer than a C5 call); released by ssb_host_release().  A concurrent call on
+// the same device gets its own temporary ring.
+struct StageCache {
+  void* p = nullptr;
+  size_t bytes = 0;
+  bool busy = false;
+};
+StageCache g_stage[64];
+
+// 4 sums per thread: two 16-byte loads, one 16-byte store; a band's outputs are contiguous
+__global__ void __launch_bounds__(256) narrow_u64_u32_kernel(const uint64_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                             int64_t n) {
+  const int64_t n4 = n >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(src) + 2 * i);
+    const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(src) + 2 * i + 1);
+    __stcs(reinterpret_cast<uint4*>(dst) + i, make_uint4((uint32_t)a.x, (uint32_t)a.y, (uint32_t)b.x, (uint32_t)b.y));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) dst[(n4 << 2) + threadIdx.x] = (uint32_t)src[(n4 << 2) + threadIdx.x];
+}
+
+// Host side of the narrow wire.  A band's uint32 sums leave the device in
+// chunks of whole output rows (a few MB, SSB_HOST_CHUNK_KB) through a small
+// pinned ring, so a chunk is widened while it is still in the host's last-level
+// cache; a coordinator waits for each chunk's copy to land, worker t widens
+// chunks t, t + T, ... into the caller's array, and the issuing thread reuses a
+// ring slot only after the chunk that held it has been widened.
+struct WirePipe {
+  int device = 0, T = 1, NS = 1;   // workers, ring slots
+  int64_t n_bands = 0, band_rows = 0, out_r = 0, out_c = 0, out_ld = 0;
+  int64_t rpc = 1, cpb = 1, n_chunks = 0;  // output rows per chunk, chunks per band, chunks in all
+  uint32_t* stage = nullptr;
+  size_t slot_elems = 0;
+  uint64_t* out = nullptr;
+  std::vector<cudaEvent_t> copied;  // per slot: the chunk's device->host copy has completed
+  std::atomic<int64_t> issued{0}, landed{0};
+  std::atomic<bool> abort{false};
+  std::unique_ptr<std::atomic<int64_t>[]> prog;  // 1 + the last chunk each worker finished
+  std::vector<std::thread> threads;
+  cudaError_t coord_err = cudaSuccess;
+  std::unique_ptr<double[]> busy;  // seconds each worker spent widening (SSB_HOST_PROF)
+  double slot_wait_s = 0.0;       // seconds the issuing thread waited for a free slot
+
+  static void nap() { std::this_thread::sleep_for(std::chrono::microseconds(5)); }
+
+  void plan(int64_t chunk_elems) {
+    rpc = chunk_elems / out_c;
+    if (rpc < 1) rpc = 1;
+    if (rpc > band_rows) rpc = band_rows;
+    cpb = (band_rows + rpc - 1) / rpc;
+    const int64_t last = out_r - (n_bands - 1) * band_rows;
+    n_chunks = (n_bands - 1) * cpb + (last + rpc - 1) / rpc;
+    slot_elems = (size_t)rpc * out_c;
+  }
+  // chunk g: band, first row inside the band, rows
+  void chunk(int64_t g, int64_t& b, int64_t& r0, int64_t& nr) const {
+    b = g / cpb;
+    r0 = (g % cpb) * rpc;
+    const int64_t o0 = b * band_rows, nb = (o0 + band_rows < out_r ? o0 + band_rows : out_r) - o0;
+    nr = r0 + rpc < nb ? rpc : nb - r0;
+  }
+
+  void start() {
+    prog.reset(new std::atomic<int64_t>[T]);
+    for (int t = 0; t < T; ++t) prog[t].store(0);
+    busy.reset(new double[T]());
+    threads.emplace_back([this] {
+      cudaSetDevice(device);
+      for (int64_t g = 0; g < n_chunks; ++g) {
+        while (issued.load(std::memory_order_acquire) <= g && !abort.load()) nap();
+        if (abort.load()) return;
+        const cudaError_t e = cudaEventSynchronize(copied[g % NS]);
+        if (e != cudaSuccess) { coord_err = e; abort.store(true); return; }
+        landed.store(g + 1, std::memory_order_release);
+      }
+    });
+    for (int t = 0; t < T; ++t)
+      threads.emplace_back([this, t] {
+        for (int64_t g = t; g < n_chunks; g += T) {
+          while (landed.load(std::memory_order_acquire) <= g && !abort.load()) nap();
+          if (abort.load()) return;
+          int64_t b, r0, nr;
+          chunk(g, b, r0, nr);
+          const uint32_t* src = stage + (size_t)(g % NS) * slot_elems;
+          uint64_t* dst = out + (size_t)(b * band_rows + r0) * out_ld;
+          const auto t0 = std::chrono::steady_clock::now();
+          if (out_ld == out_c) {
+            widen_u32_to_u64(src, dst, (size_t)nr * out_c);
+          } else {
+            for (int64_t r = 0; r < nr; ++r) widen_u32_to_u64(src + (size_t)r * out_c, dst + (size_t)r * out_ld, (size_t)out_c);
+          }
+          busy[t] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          prog[t].store(g + 1, std::memory_order_release);
+        }
+      });
+  }
+  // the slot of chunk g is free once chunk g - NS has been widened
+  bool wait_slot(int64_t g) {
+    if (g < NS) return true;
+    const int64_t prev = g - NS;
+    std::atomic<int64_t>& p = prog[prev % T];
+    if (p.load(std::memory_order_acquire) > prev) return true;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (p.load(std::memory_order_acquire) <= prev) {
+      if (abort.load()) return false;
+      nap();
+    }
+    slot_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return true;
+  }
+  void finish(bool ok) {
+    if (!ok) abort.store(true);
+    for (auto& th : threads) th.join();
+    threads.clear();
+  }
+};
 }  // namespace
 
 extern "C" {
@@ -496,7 +626,29 @@ int ssb_host_release(void) {
       cudaError_t e = cudaMemPoolTrimTo(p, 0);
       if (e != cudaSuccess) return cuda_fail(e, "ssb_host_release");
     }
+  for (auto& c : g_stage)
+    if (c.p && !c.busy) {
+      cudaFreeHost(c.p);
+      c = StageCache{};
+    }
   return SSB_OK;
+}
+
+int ssb_host_wire(int bits) {
+  const int prev = g_host_wire.load();
+  if (bits == 0 || bits == 64) g_host_wire.store(bits);
+  return prev;
+}
+
+int ssb_host_threads(int n) {
+  const int prev = g_host_threads.load();
+  if (n >= 0) g_host_threads.store(n > 64 ? 64 : n);
+  return prev;
+}
+
+void ssb_host_last_copy_bytes(int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  if (h2d_bytes) *h2d_bytes = t_host_h2d.load();
+  if (d2h_bytes) *d2h_bytes = t_host_d2h.load();
 }
 
 
@@ -551,13 +703,21 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   const size_t sat_bytes = pipeline == SSB_PIPE_TABLE ? (size_t)(max_in_rows + 1) * sat_ld * 8 : 0;
   const size_t ws_bytes = pipeline == SSB_PIPE_TABLE ? (size_t)sat_workspace_bytes(in_dtype, max_in_rows, cols, sq) : 0;
   const size_t out_bytes = (size_t)band_rows * out_c * 8;
+  // narrow wire: unsigned sums that provably fit 32 bits cross PCIe as uint32
+  // and are widened into the caller's uint64 array by host threads
+  // (host_widen.cpp); small results are not worth the threads
+  const double maxv = in_dtype == SSB_U8 ? 255.0 : in_dtype == SSB_U16 ? 65535.0 : 0.0;
+  const bool narrow = g_host_wire.load() != 64 && (stat_mask & SSB_SUM) && out_sum_host && maxv > 0.0 &&
+                      (double)w * (double)w * maxv < 4294967296.0 && out_r * out_c >= (int64_t(1) << 22);
+  t_host_h2d = rows * cols * es;
+  t_host_d2h = out_r * out_c * (8 * (nstats - 1) + ((stat_mask & SSB_SUM) ? (narrow ? 4 : 8) : 8));
 
   struct Set {
     cudaStream_t st = nullptr;         // H2D + compute of this set's bands
     cudaEvent_t ready = nullptr;       // band results complete (recorded on st)
     cudaEvent_t drained = nullptr;     // band results copied out (recorded on the D2H stream)
     void *in = nullptr, *sat = nullptr, *sq = nullptr, *ws = nullptr, *o_sum = nullptr, *o_mean = nullptr,
-         *o_std = nullptr;
+         *o_std = nullptr, *o_n32 = nullptr;
   };
   std::vector<Set> sets(n_sets);
   // every D2H goes through ONE stream in band order: the result copy is the
@@ -589,25 +749,69 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (!alloc(&s.in, in_bytes, s.st) || !alloc(&s.sat, sat_bytes, s.st) || !alloc(&s.sq, sq ? sat_bytes : 0, s.st) ||
         !alloc(&s.ws, ws_bytes, s.st) || !alloc(&s.o_sum, (stat_mask & SSB_SUM) ? out_bytes : 0, s.st) ||
         !alloc(&s.o_mean, (stat_mask & SSB_MEAN) ? out_bytes : 0, s.st) ||
-        !alloc(&s.o_std, (stat_mask & SSB_STD) ? out_bytes : 0, s.st))
+        !alloc(&s.o_std, (stat_mask & SSB_STD) ? out_bytes : 0, s.st) || !alloc(&s.o_n32, narrow ? out_bytes / 2 : 0, s.st))
       break;
+  }
+  WirePipe pipe;
+  StageCache* cache = nullptr;  // the device's cached ring when this call holds it
+  void* own_stage = nullptr;    // a temporary ring otherwise
+  if (narrow && status == SSB_OK) {
+    // widening threads: ssb_host_threads(), else SSB_HOST_THREADS, else this process's share of the
+    // cores (one process per GPU under torchrun: LOCAL_WORLD_SIZE) minus the issuing thread and the coordinator
+    static const int env_t = [] { const char* v = getenv("SSB_HOST_THREADS"); return v ? atoi(v) : 0; }();
+    static const int env_lws = [] { const char* v = getenv("LOCAL_WORLD_SIZE"); const int n = v ? atoi(v) : 1; return n < 1 ? 1 : n; }();
+    const int hw = (int)std::thread::hardware_concurrency() / env_lws;
+    const int set_t = g_host_threads.load();
+    pipe.device = device;
+    pipe.T = set_t > 0 ? set_t : env_t > 0 ? env_t : (hw > 3 ? hw - 2 : 1);
+    if (pipe.T > 64) pipe.T = 64;
+    pipe.n_bands = n_bands; pipe.band_rows = band_rows; pipe.out_r = out_r; pipe.out_c = out_c; pipe.out_ld = out_ld;
+    static const int env_kb = [] { const char* v = getenv("SSB_HOST_CHUNK_KB"); return v ? atoi(v) : 0; }();
+    pipe.plan((int64_t)(env_kb > 0 ? env_kb : 2048) * 256);  // uint32 elements per chunk
+    pipe.NS = pipe.T + 4;
+    if (pipe.NS > pipe.n_chunks) pipe.NS = (int)pipe.n_chunks;
+    pipe.out = reinterpret_cast<uint64_t*>(out_sum_host);
+    const size_t need = pipe.slot_elems * 4 * pipe.NS;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      StageCache& c = g_stage[device];
+      if (!c.busy) {
+        if (c.bytes < need) {
+          if (c.p) cudaFreeHost(c.p);
+          c = StageCache{};
+          if ((e = cudaHostAlloc(&c.p, need, cudaHostAllocDefault)) == cudaSuccess) c.bytes = need;
+          else { c.p = nullptr; status = cuda_fail(e, "pinned staging"); }
+        }
+        if (c.p) { c.busy = true; cache = &c; pipe.stage = reinterpret_cast<uint32_t*>(c.p); }
+      }
+    }
+    if (!cache && status == SSB_OK) {
+      if ((e = cudaHostAlloc(&own_stage, need, cudaHostAllocDefault)) != cudaSuccess) status = cuda_fail(e, "pinned staging");
+      pipe.stage = reinterpret_cast<uint32_t*>(own_stage);
+    }
+    pipe.copied.assign(pipe.NS, nullptr);
+    for (auto& ev : pipe.copied)
+      if (status == SSB_OK && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+        status = cuda_fail(e, "event");
+    if (status == SSB_OK) pipe.start();
   }
   if (status == SSB_OK && (e = cudaMalloc(&d_flag, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
   if (status == SSB_OK && (e = cudaMemset(d_flag, 0, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
 
-  for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
+  // one band's host->device copy and kernels on its set's stream
+  auto compute_band = [&](int64_t b) -> bool {
     Set& s = sets[b % n_sets];
     const int64_t o0 = b * band_rows, o1 = (o0 + band_rows < out_r) ? o0 + band_rows : out_r;
     const int64_t nb = o1 - o0, r0 = o0 * stride, nr = in_rows_for(nb);
     const char* src = reinterpret_cast<const char*>(in_host) + (size_t)r0 * in_ld * es;
     // the set's outputs may be overwritten once its previous band is copied out
-    if (b >= n_sets && (e = cudaStreamWaitEvent(s.st, s.drained, 0)) != cudaSuccess) { status = cuda_fail(e, "wait"); break; }
+    if (b >= n_sets && (e = cudaStreamWaitEvent(s.st, s.drained, 0)) != cudaSuccess) { status = cuda_fail(e, "wait"); return false; }
     const void* band_in = s.in;
     // contiguous rows: one linear copy (no per-row DMA descriptors)
     e = in_ld == cols ? cudaMemcpyAsync(s.in, src, (size_t)nr * cols * es, cudaMemcpyHostToDevice, s.st)
                       : cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es,
                                           (size_t)nr, cudaMemcpyHostToDevice, s.st);
-    if (e != cudaSuccess) { status = cuda_fail(e, "H2D"); break; }
+    if (e != cudaSuccess) { status = cuda_fail(e, "H2D"); return false; }
     WinOut o{s.o_sum, reinterpret_cast<double*>(s.o_mean), reinterpret_cast<double*>(s.o_std), out_c};
     if (pipeline == SSB_PIPE_TABLE && sweep_ok) {  // table + windows without reading the table back
       e = launch_sat_sweep(in_dtype, band_in, nr, cols, cols, s.sat, sat_ld, w, stat_mask, o, s.ws, s.st, false);
@@ -618,11 +822,22 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     } else {
       e = launch_window_fused(band_in, in_dtype, nr, cols, cols, w, stat_mask, o, d_flag, 0, s.st);
     }
-    if (e != cudaSuccess) { status = cuda_fail(e, "band compute"); break; }
-    if ((e = cudaEventRecord(s.ready, s.st)) != cudaSuccess || (e = cudaStreamWaitEvent(d2h_st, s.ready, 0)) != cudaSuccess) {
-      status = cuda_fail(e, "event");
-      break;
+    if (e != cudaSuccess) { status = cuda_fail(e, "band compute"); return false; }
+    if (narrow) {
+      narrow_u64_u32_kernel<<<kNumSMs * 8, 256, 0, s.st>>>(reinterpret_cast<const uint64_t*>(s.o_sum),
+                                                           reinterpret_cast<uint32_t*>(s.o_n32), nb * out_c);
+      note_launch(1);
+      if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
     }
+    if ((e = cudaEventRecord(s.ready, s.st)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
+    return true;
+  };
+  // the band's results to the host on the one copy stream
+  auto drain_band = [&](int64_t b) -> bool {
+    Set& s = sets[b % n_sets];
+    const int64_t o0 = b * band_rows, o1 = (o0 + band_rows < out_r) ? o0 + band_rows : out_r;
+    const int64_t nb = o1 - o0;
+    if ((e = cudaStreamWaitEvent(d2h_st, s.ready, 0)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
     auto d2h = [&](void* host, void* dev) -> bool {
       if (!host) return true;
       char* dst = reinterpret_cast<char*>(host) + (size_t)o0 * out_ld * 8;
@@ -633,12 +848,38 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       if (ce != cudaSuccess) { status = cuda_fail(ce, "D2H"); return false; }
       return true;
     };
-    if (!d2h((stat_mask & SSB_SUM) ? out_sum_host : nullptr, s.o_sum) ||
+    if (narrow) {
+      // chunk by chunk into the staging ring (a slot is free once the chunk that held it is widened);
+      // each landed chunk is handed to the host threads
+      for (int64_t k = 0; k * pipe.rpc < nb; ++k) {
+        const int64_t g = b * pipe.cpb + k, r0 = k * pipe.rpc, nr = r0 + pipe.rpc < nb ? pipe.rpc : nb - r0;
+        if (!pipe.wait_slot(g)) { status = fail(SSB_ECUDA, "host widening stopped"); return false; }
+        const int slot = (int)(g % pipe.NS);
+        if ((e = cudaMemcpyAsync(pipe.stage + (size_t)slot * pipe.slot_elems,
+                                 reinterpret_cast<const uint32_t*>(s.o_n32) + (size_t)r0 * out_c, (size_t)nr * out_c * 4,
+                                 cudaMemcpyDeviceToHost, d2h_st)) != cudaSuccess ||
+            (e = cudaEventRecord(pipe.copied[slot], d2h_st)) != cudaSuccess) {
+          status = cuda_fail(e, "D2H");
+          return false;
+        }
+        pipe.issued.store(g + 1, std::memory_order_release);
+      }
+    }
+    if (!d2h((stat_mask & SSB_SUM) && !narrow ? out_sum_host : nullptr, s.o_sum) ||
         !d2h((stat_mask & SSB_MEAN) ? out_mean_host : nullptr, s.o_mean) ||
         !d2h((stat_mask & SSB_STD) ? out_std_host : nullptr, s.o_std))
-      break;
-    if ((e = cudaEventRecord(s.drained, d2h_st)) != cudaSuccess) { status = cuda_fail(e, "event"); break; }
+      return false;
+    if ((e = cudaEventRecord(s.drained, d2h_st)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
+    return true;
+  };
+  // The narrow wire's drain blocks the issuing thread on ring slots for about
+  // as long as the band's copy takes, so the next band's upload and kernels
+  // are enqueued first; the straight copy never blocks.
+  for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
+    if (!compute_band(b)) break;
+    if (narrow ? (b >= 1 && !drain_band(b - 1)) : !drain_band(b)) break;
   }
+  if (narrow && status == SSB_OK) drain_band(n_bands - 1);
   if (d2h_st) {
     cudaError_t se = cudaStreamSynchronize(d2h_st);
     if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");
@@ -647,7 +888,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (!s.st) continue;
     cudaError_t se = cudaStreamSynchronize(s.st);
     if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");
-    void* ptrs[] = {s.in, s.sat, s.sq, s.ws, s.o_sum, s.o_mean, s.o_std};
+    void* ptrs[] = {s.in, s.sat, s.sq, s.ws, s.o_sum, s.o_mean, s.o_std, s.o_n32};
     for (void* p : ptrs) if (p) cudaFreeAsync(p, s.st);
     cudaStreamSynchronize(s.st);
     if (s.ready) cudaEventDestroy(s.ready);
@@ -655,6 +896,20 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     cudaStreamDestroy(s.st);
   }
   if (d2h_st) cudaStreamDestroy(d2h_st);
+  if (narrow) {
+    if (!pipe.threads.empty()) pipe.finish(status == SSB_OK);  // joins after the last band is widened
+    if (pipe.coord_err != cudaSuccess && status == SSB_OK) status = cuda_fail(pipe.coord_err, "D2H wait");
+    static const bool prof = getenv("SSB_HOST_PROF") != nullptr;  // tuning: where the host side spends its time
+    if (prof && pipe.busy) {
+      double mx = 0, sum = 0;
+      for (int t = 0; t < pipe.T; ++t) { sum += pipe.busy[t]; if (pipe.busy[t] > mx) mx = pipe.busy[t]; }
+      fprintf(stderr, "ssb_swa_host wire: T=%d slots=%d chunks=%lld x %lld rows, widen busy max %.3f s mean %.3f s, slot wait %.3f s\n", pipe.T,
+              pipe.NS, (long long)pipe.n_chunks, (long long)pipe.rpc, mx, sum / pipe.T, pipe.slot_wait_s);
+    }
+    for (auto ev : pipe.copied) if (ev) cudaEventDestroy(ev);
+    if (own_stage) cudaFreeHost(own_stage);
+    if (cache) { std::lock_guard<std::mutex> lk(g_pool_mu); cache->busy = false; }
+  }
   // the freed band buffers stay reserved in the library's pool for the next
   // call (mapping ~9 GB of fresh device memory costs ~0.1 s per C5 call);
   // ssb_host_release() returns them.  Errors trim it right away.

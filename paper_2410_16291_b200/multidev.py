@@ -21,6 +21,7 @@ rule:
 from __future__ import annotations
 
 import ctypes
+import os
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -106,8 +107,13 @@ def swa_host(img: ImageGrid, w: int, stride: int, stats, devices, pipeline: str 
     if len(parts) == 1:
         codes = [band(0)]
     else:
-        with ThreadPoolExecutor(len(parts)) as ex:
-            codes = list(ex.map(band, range(len(parts))))
+        # the concurrent calls share the host cores for widening narrow-wire results
+        prev = lib.ssb_host_threads(max(1, (os.cpu_count() or 2) // len(parts) - 1))
+        try:
+            with ThreadPoolExecutor(len(parts)) as ex:
+                codes = list(ex.map(band, range(len(parts))))
+        finally:
+            lib.ssb_host_threads(prev)
     for rc in codes:
         _lib.check(rc, "swa")
     return outs
