@@ -232,6 +232,40 @@ def test_c5_onepass_kernel_whole(sb, pool):
     del sat, outs, x
 
 
+def test_c5_host_path_whole(sb, pool):
+    """bench.py's e2e call at full C5 -- swa(pinned numpy, out=pinned) through
+    ssb_swa_host (banded upload, table + windows per band, the sums over PCIe
+    as uint32 and widened into the uint64 result by the library's host
+    threads): the whole 69,745 x 84,745 host result bit-exact against the
+    banded oracle, and the bytes that crossed PCIe."""
+    import ctypes
+
+    import torch
+
+    from paper_2410_16291_b200 import _lib, synthetic
+
+    lib = _lib.load()
+    img = synthetic.c5(threads=P)
+    hin = torch.empty(img.shape, dtype=torch.uint8, pin_memory=True)
+    hin.numpy()[...] = img
+    out_r, out_c = 70000 - 255, 85000 - 255
+    hout = torch.empty((out_r, out_c), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+    hout[...] = 0xDEADBEEFDEADBEEF
+    lib.ssb_host_wire(0)
+    got = sb.swa(hin.numpy(), 256, "sum", pipeline="table", out=hout, devices=[0])
+    assert got is hout or np.shares_memory(got, hout)
+    h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
+    lib.ssb_host_last_copy_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
+    assert (h2d.value, d2h.value) == (70000 * 85000, 4 * out_r * out_c)
+    for lo in range(0, out_r, 4096):
+        hi = min(out_r, lo + 4096)
+        ref = O.swa_threaded(img[lo:hi + 255], 256, "sum", 1, P)
+        assert par_equal(hout[lo:hi], ref.astype(np.uint64, copy=False), pool), f"host sums rows {lo}..{hi} differ"
+        del ref
+    del hout, hin
+    lib.ssb_host_release()
+
+
 # ----------------------------------------------------------------------------- C4 (float)
 @pytest.mark.parametrize("pipe", ["table", "fused"])
 def test_c4_whole_mean_std(sb, pool, pipe):
