@@ -270,11 +270,13 @@ int ssb_host_release(void);
 /* Wire format of ssb_swa_host's SUM results (api.py:28-55 returns uint64 on
  * the host; the device->host copy of the results is the end-to-end critical
  * path).  0 (default): when every sum provably fits 32 bits (unsigned pixels,
- * w^2 * max pixel < 2^32) the device narrows the sums to uint32 before the
- * copy and the library's host threads zero-extend each landed band into the
- * caller's uint64 array -- half the PCIe bytes, the same values; every other
- * case copies 64-bit results straight into the caller's array.  64: always
- * the straight copy.  Returns the previous setting; other values only query. */
+ * w^2 * max pixel < 2^32) the device narrows the sums before the copy -- to
+ * uint32, or to uint16 for a band whose largest sum (computed on the device)
+ * is below 2^16 -- and the library's host threads zero-extend each landed
+ * chunk into the caller's uint64 array: a half or a quarter of the PCIe
+ * bytes, the same values; every other case copies 64-bit results straight
+ * into the caller's array.  32: never narrower than uint32.  64: always the
+ * straight copy.  Returns the previous setting; other values only query. */
 int ssb_host_wire(int bits);
 
 /* Host threads each ssb_swa_host call uses to widen narrow-wire results

@@ -22,6 +22,7 @@
 
 namespace ssb {
 void widen_u32_to_u64(const uint32_t* src, uint64_t* dst, size_t n);  // host_widen.cpp
+void widen_u16_to_u64(const uint16_t* src, uint64_t* dst, size_t n);
 }
 
 #ifndef SSB_ENONFINITE
@@ -396,16 +397,40 @@ struct StageCache {
 };
 StageCache g_stage[64];
 
-// 4 sums per thread: two 16-byte loads, one 16-byte store; a band's outputs are contiguous
+// 4 sums per thread: two 16-byte loads, one 16-byte store; a band's outputs are
+// contiguous.  *band_max receives the band's largest sum (one atomic per warp):
+// a band whose sums all fit 16 bits leaves as uint16 instead.
 __global__ void __launch_bounds__(256) narrow_u64_u32_kernel(const uint64_t* __restrict__ src, uint32_t* __restrict__ dst,
-                                                             int64_t n) {
+                                                             int64_t n, uint32_t* __restrict__ band_max) {
   const int64_t n4 = n >> 2;
+  uint32_t mx = 0u;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(src) + 2 * i);
     const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(src) + 2 * i + 1);
-    __stcs(reinterpret_cast<uint4*>(dst) + i, make_uint4((uint32_t)a.x, (uint32_t)a.y, (uint32_t)b.x, (uint32_t)b.y));
+    const uint4 v = make_uint4((uint32_t)a.x, (uint32_t)a.y, (uint32_t)b.x, (uint32_t)b.y);
+    mx = max(max(mx, max(v.x, v.y)), max(v.z, v.w));
+    __stcs(reinterpret_cast<uint4*>(dst) + i, v);
   }
-  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) dst[(n4 << 2) + threadIdx.x] = (uint32_t)src[(n4 << 2) + threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const uint32_t v = (uint32_t)src[(n4 << 2) + threadIdx.x];
+    dst[(n4 << 2) + threadIdx.x] = v;
+    mx = max(mx, v);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(band_max, mx);
+}
+
+// 8 sums per thread (32-byte load, 16-byte store); only for bands whose largest sum fits 16 bits
+__global__ void __launch_bounds__(256) narrow_u32_u16_kernel(const uint32_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                                             int64_t n) {
+  const int64_t n8 = n >> 3;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(src) + 2 * i);
+    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(src) + 2 * i + 1);
+    __stcs(reinterpret_cast<uint4*>(dst) + i,
+           make_uint4(a.x | (a.y << 16), a.z | (a.w << 16), b.x | (b.y << 16), b.z | (b.w << 16)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 7)) dst[(n8 << 3) + threadIdx.x] = (uint16_t)src[(n8 << 3) + threadIdx.x];
 }
 
 // Host side of the narrow wire.  A band's uint32 sums leave the device in
@@ -420,6 +445,8 @@ struct WirePipe {
   int64_t rpc = 1, cpb = 1, n_chunks = 0;  // output rows per chunk, chunks per band, chunks in all
   uint32_t* stage = nullptr;
   size_t slot_elems = 0;
+  std::vector<unsigned char> fmt16;  // per slot: the chunk it holds is uint16 (else uint32)
+  int64_t copied_bytes = 0;          // device->host bytes of the narrow chunks (issuing thread)
   uint64_t* out = nullptr;
   std::vector<cudaEvent_t> copied;  // per slot: the chunk's device->host copy has completed
   std::atomic<int64_t> issued{0}, landed{0};
@@ -471,12 +498,18 @@ struct WirePipe {
           int64_t b, r0, nr;
           chunk(g, b, r0, nr);
           const uint32_t* src = stage + (size_t)(g % NS) * slot_elems;
+          const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
           uint64_t* dst = out + (size_t)(b * band_rows + r0) * out_ld;
+          const bool h = fmt16[g % NS] != 0;  // written before `issued`, read after `landed`
           const auto t0 = std::chrono::steady_clock::now();
           if (out_ld == out_c) {
-            widen_u32_to_u64(src, dst, (size_t)nr * out_c);
+            if (h) widen_u16_to_u64(src16, dst, (size_t)nr * out_c);
+            else widen_u32_to_u64(src, dst, (size_t)nr * out_c);
           } else {
-            for (int64_t r = 0; r < nr; ++r) widen_u32_to_u64(src + (size_t)r * out_c, dst + (size_t)r * out_ld, (size_t)out_c);
+            for (int64_t r = 0; r < nr; ++r) {
+              if (h) widen_u16_to_u64(src16 + (size_t)r * out_c, dst + (size_t)r * out_ld, (size_t)out_c);
+              else widen_u32_to_u64(src + (size_t)r * out_c, dst + (size_t)r * out_ld, (size_t)out_c);
+            }
           }
           busy[t] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
           prog[t].store(g + 1, std::memory_order_release);
@@ -636,7 +669,7 @@ int ssb_host_release(void) {
 
 int ssb_host_wire(int bits) {
   const int prev = g_host_wire.load();
-  if (bits == 0 || bits == 64) g_host_wire.store(bits);
+  if (bits == 0 || bits == 32 || bits == 64) g_host_wire.store(bits);
   return prev;
 }
 
@@ -709,6 +742,8 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   const double maxv = in_dtype == SSB_U8 ? 255.0 : in_dtype == SSB_U16 ? 65535.0 : 0.0;
   const bool narrow = g_host_wire.load() != 64 && (stat_mask & SSB_SUM) && out_sum_host && maxv > 0.0 &&
                       (double)w * (double)w * maxv < 4294967296.0 && out_r * out_c >= (int64_t(1) << 22);
+  const bool allow16 = g_host_wire.load() != 32;
+  uint32_t* h_max = nullptr;  // pinned: the bands' largest sums, one word per buffer set (tail of the ring)
   t_host_h2d = rows * cols * es;
   t_host_d2h = out_r * out_c * (8 * (nstats - 1) + ((stat_mask & SSB_SUM) ? (narrow ? 4 : 8) : 8));
 
@@ -718,6 +753,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     cudaEvent_t drained = nullptr;     // band results copied out (recorded on the D2H stream)
     void *in = nullptr, *sat = nullptr, *sq = nullptr, *ws = nullptr, *o_sum = nullptr, *o_mean = nullptr,
          *o_std = nullptr, *o_n32 = nullptr;
+    uint32_t* d_max = nullptr;  // the band's largest sum (narrow wire)
   };
   std::vector<Set> sets(n_sets);
   // every D2H goes through ONE stream in band order: the result copy is the
@@ -749,7 +785,8 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (!alloc(&s.in, in_bytes, s.st) || !alloc(&s.sat, sat_bytes, s.st) || !alloc(&s.sq, sq ? sat_bytes : 0, s.st) ||
         !alloc(&s.ws, ws_bytes, s.st) || !alloc(&s.o_sum, (stat_mask & SSB_SUM) ? out_bytes : 0, s.st) ||
         !alloc(&s.o_mean, (stat_mask & SSB_MEAN) ? out_bytes : 0, s.st) ||
-        !alloc(&s.o_std, (stat_mask & SSB_STD) ? out_bytes : 0, s.st) || !alloc(&s.o_n32, narrow ? out_bytes / 2 : 0, s.st))
+        !alloc(&s.o_std, (stat_mask & SSB_STD) ? out_bytes : 0, s.st) || !alloc(&s.o_n32, narrow ? out_bytes / 2 : 0, s.st) ||
+        !alloc(reinterpret_cast<void**>(&s.d_max), narrow ? 256 : 0, s.st))
       break;
   }
   WirePipe pipe;
@@ -771,7 +808,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     pipe.NS = pipe.T + 4;
     if (pipe.NS > pipe.n_chunks) pipe.NS = (int)pipe.n_chunks;
     pipe.out = reinterpret_cast<uint64_t*>(out_sum_host);
-    const size_t need = pipe.slot_elems * 4 * pipe.NS;
+    const size_t need = pipe.slot_elems * 4 * pipe.NS + 256;  // + the bands' maxima (one word per buffer set)
     {
       std::lock_guard<std::mutex> lk(g_pool_mu);
       StageCache& c = g_stage[device];
@@ -789,6 +826,8 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       if ((e = cudaHostAlloc(&own_stage, need, cudaHostAllocDefault)) != cudaSuccess) status = cuda_fail(e, "pinned staging");
       pipe.stage = reinterpret_cast<uint32_t*>(own_stage);
     }
+    if (pipe.stage) h_max = pipe.stage + pipe.slot_elems * pipe.NS;
+    pipe.fmt16.assign(pipe.NS, 0);
     pipe.copied.assign(pipe.NS, nullptr);
     for (auto& ev : pipe.copied)
       if (status == SSB_OK && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
@@ -824,10 +863,15 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     }
     if (e != cudaSuccess) { status = cuda_fail(e, "band compute"); return false; }
     if (narrow) {
+      if ((e = cudaMemsetAsync(s.d_max, 0, 4, s.st)) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
       narrow_u64_u32_kernel<<<kNumSMs * 8, 256, 0, s.st>>>(reinterpret_cast<const uint64_t*>(s.o_sum),
-                                                           reinterpret_cast<uint32_t*>(s.o_n32), nb * out_c);
+                                                           reinterpret_cast<uint32_t*>(s.o_n32), nb * out_c, s.d_max);
       note_launch(1);
-      if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
+      if ((e = cudaGetLastError()) != cudaSuccess ||
+          (e = cudaMemcpyAsync(h_max + (b % n_sets), s.d_max, 4, cudaMemcpyDeviceToHost, s.st)) != cudaSuccess) {
+        status = cuda_fail(e, "narrow");
+        return false;
+      }
     }
     if ((e = cudaEventRecord(s.ready, s.st)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
     return true;
@@ -849,15 +893,28 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       return true;
     };
     if (narrow) {
+      // a band whose largest sum fits 16 bits leaves as uint16 (decided from the band's maximum, which
+      // the narrowing kernel computed; the issuing thread runs ahead of the device, so this wait is short)
+      if ((e = cudaEventSynchronize(s.ready)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
+      const bool half = allow16 && h_max[b % n_sets] < 65536u;
+      const int esz = half ? 2 : 4;
+      if (half) {  // the uint64 sums are dead once narrowed: their buffer takes the uint16 copy
+        narrow_u32_u16_kernel<<<kNumSMs * 8, 256, 0, d2h_st>>>(reinterpret_cast<const uint32_t*>(s.o_n32),
+                                                               reinterpret_cast<uint16_t*>(s.o_sum), nb * out_c);
+        note_launch(1);
+        if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
+      }
+      const char* band_src = reinterpret_cast<const char*>(half ? s.o_sum : s.o_n32);
       // chunk by chunk into the staging ring (a slot is free once the chunk that held it is widened);
       // each landed chunk is handed to the host threads
       for (int64_t k = 0; k * pipe.rpc < nb; ++k) {
         const int64_t g = b * pipe.cpb + k, r0 = k * pipe.rpc, nr = r0 + pipe.rpc < nb ? pipe.rpc : nb - r0;
         if (!pipe.wait_slot(g)) { status = fail(SSB_ECUDA, "host widening stopped"); return false; }
         const int slot = (int)(g % pipe.NS);
-        if ((e = cudaMemcpyAsync(pipe.stage + (size_t)slot * pipe.slot_elems,
-                                 reinterpret_cast<const uint32_t*>(s.o_n32) + (size_t)r0 * out_c, (size_t)nr * out_c * 4,
-                                 cudaMemcpyDeviceToHost, d2h_st)) != cudaSuccess ||
+        pipe.fmt16[slot] = half ? 1 : 0;
+        pipe.copied_bytes += nr * out_c * esz;
+        if ((e = cudaMemcpyAsync(pipe.stage + (size_t)slot * pipe.slot_elems, band_src + (size_t)r0 * out_c * esz,
+                                 (size_t)nr * out_c * esz, cudaMemcpyDeviceToHost, d2h_st)) != cudaSuccess ||
             (e = cudaEventRecord(pipe.copied[slot], d2h_st)) != cudaSuccess) {
           status = cuda_fail(e, "D2H");
           return false;
@@ -888,7 +945,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (!s.st) continue;
     cudaError_t se = cudaStreamSynchronize(s.st);
     if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");
-    void* ptrs[] = {s.in, s.sat, s.sq, s.ws, s.o_sum, s.o_mean, s.o_std, s.o_n32};
+    void* ptrs[] = {s.in, s.sat, s.sq, s.ws, s.o_sum, s.o_mean, s.o_std, s.o_n32, s.d_max};
     for (void* p : ptrs) if (p) cudaFreeAsync(p, s.st);
     cudaStreamSynchronize(s.st);
     if (s.ready) cudaEventDestroy(s.ready);
@@ -898,6 +955,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   if (d2h_st) cudaStreamDestroy(d2h_st);
   if (narrow) {
     if (!pipe.threads.empty()) pipe.finish(status == SSB_OK);  // joins after the last band is widened
+    t_host_d2h = out_r * out_c * 8 * (nstats - 1) + pipe.copied_bytes;
     if (pipe.coord_err != cudaSuccess && status == SSB_OK) status = cuda_fail(pipe.coord_err, "D2H wait");
     static const bool prof = getenv("SSB_HOST_PROF") != nullptr;  // tuning: where the host side spends its time
     if (prof && pipe.busy) {

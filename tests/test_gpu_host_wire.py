@@ -98,7 +98,39 @@ def test_narrow_sum_with_wide_mean(lib):
     got, avg, _, d2h = host_sum(lib, img, 50, band_rows=256, mean=True)
     assert np.array_equal(got, O.swa(img, 50, "sum"))
     assert np.array_equal(avg, O.swa(img, 50, "mean"))
-    assert d2h == 12 * got.size
+    assert d2h == 10 * got.size  # sums <= 2500: uint16 on the wire; means float64
+
+
+def test_uint16_wire_per_band(lib):
+    """A band whose largest sum is below 2^16 leaves as uint16, the others as uint32 (decided per band
+    from the device-computed maximum); ssb_host_wire(32) keeps every band at uint32."""
+    rng = np.random.default_rng(5)
+    img = (rng.random((2600, 2500)) < 0.2).astype(np.uint8)
+    img[1500:1900, 700:1400] = 255  # sums far above 65535 in the bands that see this block
+    w, br = 40, 400
+    ref = O.swa(img, w, "sum")
+    out_r, out_c = ref.shape
+    lib.ssb_host_wire(0)
+    got, _, _, d2h = host_sum(lib, img, w, band_rows=br)
+    assert np.array_equal(got, ref)
+    expect = sum((min(out_r, lo + br) - lo) * out_c * (2 if ref[lo:lo + br].max() < 65536 else 4)
+                 for lo in range(0, out_r, br))
+    assert 2 * ref.size < expect < 4 * ref.size and d2h == expect
+    # exactly 65535 still fits (one zero in every 256 x 256 window), 65536 does not
+    edge = np.ones((2304, 2304), dtype=np.uint8)
+    edge[::256, ::256] = 0
+    got, _, _, d2h = host_sum(lib, edge, 256, band_rows=600)
+    assert (got == 65535).all() and d2h == 2 * got.size
+    one = np.ones((2200, 2200), dtype=np.uint8)
+    got, _, _, d2h = host_sum(lib, one, 256, band_rows=500)  # every sum == 65536: one above uint16
+    assert (got == 65536).all() and d2h == 4 * got.size
+    one[::7, ::5] = 0
+    got, _, _, d2h = host_sum(lib, one, 255, band_rows=500)  # <= 65025
+    assert np.array_equal(got, O.swa(one, 255, "sum")) and d2h == 2 * got.size
+    assert lib.ssb_host_wire(32) == 0
+    got, _, _, d2h = host_sum(lib, img, w, band_rows=br)
+    assert np.array_equal(got, ref) and d2h == 4 * ref.size
+    assert lib.ssb_host_wire(0) == 32
 
 
 def test_public_api_host_arrays(lib):
