@@ -440,16 +440,21 @@ __global__ void __launch_bounds__(256) narrow_u32_u16_kernel(const uint32_t* __r
 // chunks t, t + T, ... into the caller's array, and the issuing thread reuses a
 // ring slot only after the chunk that held it has been widened.
 struct WirePipe {
-  int device = 0, T = 1, NS = 1;   // workers, ring slots
-  int64_t n_bands = 0, band_rows = 0, out_r = 0, out_c = 0, out_ld = 0;
-  int64_t rpc = 1, cpb = 1, n_chunks = 0;  // output rows per chunk, chunks per band, chunks in all
+  struct Desc {           // what a ring slot holds; written before `issued`, read after `landed`
+    uint64_t* dst = nullptr;  // first output row of the chunk in the caller's array
+    int64_t rows = 0;
+    bool half = false;        // uint16 (else uint32)
+  };
+  int device = 0, T = 1, NS = 1;  // workers, ring slots
+  int64_t out_c = 0, out_ld = 0;
+  int64_t rpc = 1;                // output rows per uint32 chunk (a uint16 chunk takes twice as many: the same bytes)
   uint32_t* stage = nullptr;
-  size_t slot_elems = 0;
-  std::vector<unsigned char> fmt16;  // per slot: the chunk it holds is uint16 (else uint32)
-  int64_t copied_bytes = 0;          // device->host bytes of the narrow chunks (issuing thread)
-  uint64_t* out = nullptr;
+  size_t slot_elems = 0;          // uint32 elements per slot
+  std::vector<Desc> desc;         // per slot
+  int64_t copied_bytes = 0;       // device->host bytes of the narrow chunks (issuing thread)
   std::vector<cudaEvent_t> copied;  // per slot: the chunk's device->host copy has completed
   std::atomic<int64_t> issued{0}, landed{0};
+  std::atomic<int64_t> total{-1};   // chunks in all, published once the last one is issued
   std::atomic<bool> abort{false};
   std::unique_ptr<std::atomic<int64_t>[]> prog;  // 1 + the last chunk each worker finished
   std::vector<std::thread> threads;
@@ -459,21 +464,20 @@ struct WirePipe {
 
   static void nap() { std::this_thread::sleep_for(std::chrono::microseconds(5)); }
 
-  void plan(int64_t chunk_elems) {
+  void plan(int64_t chunk_elems, int64_t band_rows) {
     rpc = chunk_elems / out_c;
     if (rpc < 1) rpc = 1;
     if (rpc > band_rows) rpc = band_rows;
-    cpb = (band_rows + rpc - 1) / rpc;
-    const int64_t last = out_r - (n_bands - 1) * band_rows;
-    n_chunks = (n_bands - 1) * cpb + (last + rpc - 1) / rpc;
     slot_elems = (size_t)rpc * out_c;
   }
-  // chunk g: band, first row inside the band, rows
-  void chunk(int64_t g, int64_t& b, int64_t& r0, int64_t& nr) const {
-    b = g / cpb;
-    r0 = (g % cpb) * rpc;
-    const int64_t o0 = b * band_rows, nb = (o0 + band_rows < out_r ? o0 + band_rows : out_r) - o0;
-    nr = r0 + rpc < nb ? rpc : nb - r0;
+  // waits until chunk g has reached `stage` (true) or no chunk g will come (false)
+  bool wait_for(const std::atomic<int64_t>& stage_count, int64_t g) {
+    for (;;) {
+      if (stage_count.load(std::memory_order_acquire) > g) return true;
+      const int64_t n = total.load(std::memory_order_acquire);
+      if ((n >= 0 && g >= n) || abort.load()) return false;
+      nap();
+    }
   }
 
   void start() {
@@ -482,9 +486,7 @@ struct WirePipe {
     busy.reset(new double[T]());
     threads.emplace_back([this] {
       cudaSetDevice(device);
-      for (int64_t g = 0; g < n_chunks; ++g) {
-        while (issued.load(std::memory_order_acquire) <= g && !abort.load()) nap();
-        if (abort.load()) return;
+      for (int64_t g = 0; wait_for(issued, g); ++g) {
         const cudaError_t e = cudaEventSynchronize(copied[g % NS]);
         if (e != cudaSuccess) { coord_err = e; abort.store(true); return; }
         landed.store(g + 1, std::memory_order_release);
@@ -492,23 +494,18 @@ struct WirePipe {
     });
     for (int t = 0; t < T; ++t)
       threads.emplace_back([this, t] {
-        for (int64_t g = t; g < n_chunks; g += T) {
-          while (landed.load(std::memory_order_acquire) <= g && !abort.load()) nap();
-          if (abort.load()) return;
-          int64_t b, r0, nr;
-          chunk(g, b, r0, nr);
+        for (int64_t g = t; wait_for(landed, g); g += T) {
+          const Desc d = desc[g % NS];
           const uint32_t* src = stage + (size_t)(g % NS) * slot_elems;
           const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
-          uint64_t* dst = out + (size_t)(b * band_rows + r0) * out_ld;
-          const bool h = fmt16[g % NS] != 0;  // written before `issued`, read after `landed`
           const auto t0 = std::chrono::steady_clock::now();
           if (out_ld == out_c) {
-            if (h) widen_u16_to_u64(src16, dst, (size_t)nr * out_c);
-            else widen_u32_to_u64(src, dst, (size_t)nr * out_c);
+            if (d.half) widen_u16_to_u64(src16, d.dst, (size_t)d.rows * out_c);
+            else widen_u32_to_u64(src, d.dst, (size_t)d.rows * out_c);
           } else {
-            for (int64_t r = 0; r < nr; ++r) {
-              if (h) widen_u16_to_u64(src16 + (size_t)r * out_c, dst + (size_t)r * out_ld, (size_t)out_c);
-              else widen_u32_to_u64(src + (size_t)r * out_c, dst + (size_t)r * out_ld, (size_t)out_c);
+            for (int64_t r = 0; r < d.rows; ++r) {
+              if (d.half) widen_u16_to_u64(src16 + (size_t)r * out_c, d.dst + (size_t)r * out_ld, (size_t)out_c);
+              else widen_u32_to_u64(src + (size_t)r * out_c, d.dst + (size_t)r * out_ld, (size_t)out_c);
             }
           }
           busy[t] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -530,8 +527,10 @@ struct WirePipe {
     slot_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return true;
   }
+  // no more chunks: the threads leave once the issued ones are widened
   void finish(bool ok) {
     if (!ok) abort.store(true);
+    total.store(issued.load(), std::memory_order_release);
     for (auto& th : threads) th.join();
     threads.clear();
   }
@@ -802,12 +801,10 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     pipe.device = device;
     pipe.T = set_t > 0 ? set_t : env_t > 0 ? env_t : (hw > 3 ? hw - 2 : 1);
     if (pipe.T > 64) pipe.T = 64;
-    pipe.n_bands = n_bands; pipe.band_rows = band_rows; pipe.out_r = out_r; pipe.out_c = out_c; pipe.out_ld = out_ld;
+    pipe.out_c = out_c; pipe.out_ld = out_ld;
     static const int env_kb = [] { const char* v = getenv("SSB_HOST_CHUNK_KB"); return v ? atoi(v) : 0; }();
-    pipe.plan((int64_t)(env_kb > 0 ? env_kb : 2048) * 256);  // uint32 elements per chunk
+    pipe.plan((int64_t)(env_kb > 0 ? env_kb : 2048) * 256, band_rows);  // uint32 elements per chunk
     pipe.NS = pipe.T + 4;
-    if (pipe.NS > pipe.n_chunks) pipe.NS = (int)pipe.n_chunks;
-    pipe.out = reinterpret_cast<uint64_t*>(out_sum_host);
     const size_t need = pipe.slot_elems * 4 * pipe.NS + 256;  // + the bands' maxima (one word per buffer set)
     {
       std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -827,7 +824,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       pipe.stage = reinterpret_cast<uint32_t*>(own_stage);
     }
     if (pipe.stage) h_max = pipe.stage + pipe.slot_elems * pipe.NS;
-    pipe.fmt16.assign(pipe.NS, 0);
+    pipe.desc.assign(pipe.NS, WirePipe::Desc{});
     pipe.copied.assign(pipe.NS, nullptr);
     for (auto& ev : pipe.copied)
       if (status == SSB_OK && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
@@ -907,11 +904,12 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       const char* band_src = reinterpret_cast<const char*>(half ? s.o_sum : s.o_n32);
       // chunk by chunk into the staging ring (a slot is free once the chunk that held it is widened);
       // each landed chunk is handed to the host threads
-      for (int64_t k = 0; k * pipe.rpc < nb; ++k) {
-        const int64_t g = b * pipe.cpb + k, r0 = k * pipe.rpc, nr = r0 + pipe.rpc < nb ? pipe.rpc : nb - r0;
+      const int64_t step = half ? 2 * pipe.rpc : pipe.rpc;  // the same bytes per chunk in either format
+      for (int64_t r0 = 0; r0 < nb; r0 += step) {
+        const int64_t g = pipe.issued.load(std::memory_order_relaxed), nr = r0 + step < nb ? step : nb - r0;
         if (!pipe.wait_slot(g)) { status = fail(SSB_ECUDA, "host widening stopped"); return false; }
         const int slot = (int)(g % pipe.NS);
-        pipe.fmt16[slot] = half ? 1 : 0;
+        pipe.desc[slot] = WirePipe::Desc{reinterpret_cast<uint64_t*>(out_sum_host) + (size_t)(o0 + r0) * out_ld, nr, half};
         pipe.copied_bytes += nr * out_c * esz;
         if ((e = cudaMemcpyAsync(pipe.stage + (size_t)slot * pipe.slot_elems, band_src + (size_t)r0 * out_c * esz,
                                  (size_t)nr * out_c * esz, cudaMemcpyDeviceToHost, d2h_st)) != cudaSuccess ||
@@ -961,8 +959,8 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (prof && pipe.busy) {
       double mx = 0, sum = 0;
       for (int t = 0; t < pipe.T; ++t) { sum += pipe.busy[t]; if (pipe.busy[t] > mx) mx = pipe.busy[t]; }
-      fprintf(stderr, "ssb_swa_host wire: T=%d slots=%d chunks=%lld x %lld rows, widen busy max %.3f s mean %.3f s, slot wait %.3f s\n", pipe.T,
-              pipe.NS, (long long)pipe.n_chunks, (long long)pipe.rpc, mx, sum / pipe.T, pipe.slot_wait_s);
+      fprintf(stderr, "ssb_swa_host wire: T=%d slots=%d chunks=%lld x %lld rows (x2 as uint16), widen busy max %.3f s mean %.3f s, slot wait %.3f s\n",
+              pipe.T, pipe.NS, (long long)pipe.issued.load(), (long long)pipe.rpc, mx, sum / pipe.T, pipe.slot_wait_s);
     }
     for (auto ev : pipe.copied) if (ev) cudaEventDestroy(ev);
     if (own_stage) cudaFreeHost(own_stage);

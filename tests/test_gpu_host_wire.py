@@ -121,7 +121,7 @@ def test_uint16_wire_per_band(lib):
     edge[::256, ::256] = 0
     got, _, _, d2h = host_sum(lib, edge, 256, band_rows=600)
     assert (got == 65535).all() and d2h == 2 * got.size
-    one = np.ones((2200, 2200), dtype=np.uint8)
+    one = np.ones((2400, 2400), dtype=np.uint8)
     got, _, _, d2h = host_sum(lib, one, 256, band_rows=500)  # every sum == 65536: one above uint16
     assert (got == 65536).all() and d2h == 4 * got.size
     one[::7, ::5] = 0
