@@ -279,6 +279,11 @@ int ssb_host_release(void);
  * straight copy.  Returns the previous setting; other values only query. */
 int ssb_host_wire(int bits);
 
+/* The host half of the narrow wire on its own: dst_u64[i] = src[i] for i < n,
+ * zero-extended from src_bits = 16 or 32 (HOST pointers, any element
+ * alignment; AVX2 streaming stores where the CPU has them).  No device work. */
+int ssb_host_widen(const void* src, int src_bits, void* dst_u64, int64_t n);
+
 /* Host threads each ssb_swa_host call uses to widen narrow-wire results
  * (0 = automatic: the process's share of the cores minus two; n > 0 fixes it,
  * e.g. cores / devices when one process drives several GPUs at once).  Returns

@@ -672,6 +672,14 @@ int ssb_host_wire(int bits) {
   return prev;
 }
 
+int ssb_host_widen(const void* src, int src_bits, void* dst_u64, int64_t n) {
+  if (!src || !dst_u64 || n < 0) return fail(SSB_EINVAL, "ssb_host_widen: bad arguments");
+  if (src_bits == 32) widen_u32_to_u64(reinterpret_cast<const uint32_t*>(src), reinterpret_cast<uint64_t*>(dst_u64), (size_t)n);
+  else if (src_bits == 16) widen_u16_to_u64(reinterpret_cast<const uint16_t*>(src), reinterpret_cast<uint64_t*>(dst_u64), (size_t)n);
+  else return fail(SSB_EINVAL, "ssb_host_widen: src_bits must be 16 or 32");
+  return SSB_OK;
+}
+
 int ssb_host_threads(int n) {
   const int prev = g_host_threads.load();
   if (n >= 0) g_host_threads.store(n > 64 ? 64 : n);

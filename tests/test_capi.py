@@ -111,3 +111,27 @@ def test_sharded_validation_without_device(lib):
     assert lib.ssb_sharded_plan(10, 10, 11, 2, (ctypes.c_int64 * 14)()) == _lib.EINVAL
     assert lib.ssb_sharded_workspace_bytes(_lib.U8, 10, 10, 3, 2, 5, 1) == -1
     assert lib.ssb_band_carry(None, 1, 10, 10, 0, None, None) == _lib.EINVAL
+
+
+def test_host_widen_and_wire_settings(lib):
+    """The host half of ssb_swa_host's narrow wire (host_widen.cpp) needs no device:
+    zero-extension of uint16 / uint32 into uint64 at every alignment and length, and
+    the wire / thread settings round-trip."""
+    import numpy as np
+
+    rng = np.random.default_rng(16)
+    for bits, dt in ((16, np.uint16), (32, np.uint32)):
+        src = rng.integers(0, 2**bits, size=5000, dtype=np.uint64).astype(dt)
+        src[:4] = [0, 2**bits - 1, 2**(bits - 1), 1]  # the top bit must not sign-extend
+        for off_s, off_d, n in ((0, 0, 5000), (1, 0, 4097), (3, 1, 1023), (2, 3, 7), (5, 2, 0), (0, 1, 1), (7, 5, 64)):
+            dst = np.full(off_d + n + 9, 0xA5A5A5A5A5A5A5A5, dtype=np.uint64)
+            s = np.ascontiguousarray(src[off_s:off_s + n])
+            rc = lib.ssb_host_widen(s.ctypes.data_as(ctypes.c_void_p), bits, ctypes.c_void_p(dst.ctypes.data + 8 * off_d), n)
+            assert rc == 0
+            assert np.array_equal(dst[off_d:off_d + n], s.astype(np.uint64))
+            assert (dst[:off_d] == 0xA5A5A5A5A5A5A5A5).all() and (dst[off_d + n:] == 0xA5A5A5A5A5A5A5A5).all()
+    one = np.zeros(1, np.uint64)
+    assert lib.ssb_host_widen(one.ctypes.data_as(ctypes.c_void_p), 8, one.ctypes.data_as(ctypes.c_void_p), 1) == _lib.EINVAL
+    assert lib.ssb_host_wire(-1) == 0 and lib.ssb_host_wire(32) == 0 and lib.ssb_host_wire(7) == 32
+    assert lib.ssb_host_wire(64) == 32 and lib.ssb_host_wire(0) == 64 and lib.ssb_host_wire(-1) == 0
+    assert lib.ssb_host_threads(-1) == 0 and lib.ssb_host_threads(5) == 0 and lib.ssb_host_threads(0) == 5
