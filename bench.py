@@ -523,6 +523,10 @@ def main() -> None:
         "clocks": clk.summary(),
     }
 
+    # rows of the timed step's window sums, kept for a cross-check of the e2e (host path) result below
+    check_rows = [0, 1, OUT_R // 3, OUT_R // 2 + 7, OUT_R - 1]
+    dev_rows = out[check_rows].cpu().numpy().view(np.uint64) if world == 1 else None
+
     if world == 1 and not args.no_extra:
         # per-kernel times in context: the same launches issued from here with
         # events around each kernel group (untimed pass)
@@ -650,6 +654,8 @@ def main() -> None:
                 dist.all_reduce(mx, op=dist.ReduceOp.MAX)
                 dist.all_reduce(agg, op=dist.ReduceOp.SUM)
                 te, h2d, d2h = float(mx.item()), int(agg[1].item()), int(agg[2].item())
+            if dev_rows is not None:  # the host path's uint64 result against the device-resident step's, row for row
+                wire["rows_equal_device_step"] = bool(np.array_equal(hout[check_rows], dev_rows))
             result["e2e"] = {"value": px / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                              "d2h_bytes_per_step": d2h, "s_per_step": te, "steps_s": times,
                              "d2h_gbs": d2h / te / 1e9, "wire": wire,

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -837,7 +838,14 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     for (auto& ev : pipe.copied)
       if (status == SSB_OK && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
         status = cuda_fail(e, "event");
-    if (status == SSB_OK) pipe.start();
+    if (status == SSB_OK) {
+      try {
+        pipe.start();
+      } catch (const std::exception& ex) {  // thread creation failed: stop the ones that started
+        pipe.finish(false);
+        status = fail(SSB_ECUDA, "host widening threads: %s", ex.what());
+      }
+    }
   }
   if (status == SSB_OK && (e = cudaMalloc(&d_flag, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
   if (status == SSB_OK && (e = cudaMemset(d_flag, 0, sizeof(int))) != cudaSuccess) status = cuda_fail(e, "flag");
