@@ -752,7 +752,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
                       (double)w * (double)w * maxv < 4294967296.0 && out_r * out_c >= (int64_t(1) << 22);
   const bool allow16 = g_host_wire.load() != 32;
   uint32_t* h_max = nullptr;  // pinned: the bands' largest sums, one word per buffer set (tail of the ring)
-  t_host_h2d = rows * cols * es;
+  int64_t h2d_bytes = 0;  // uploaded: every band's input rows (consecutive bands share w - stride rows)
   t_host_d2h = out_r * out_c * (8 * (nstats - 1) + ((stat_mask & SSB_SUM) ? (narrow ? 4 : 8) : 8));
 
   struct Set {
@@ -864,6 +864,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
                       : cudaMemcpy2DAsync(s.in, (size_t)cols * es, src, (size_t)in_ld * es, (size_t)cols * es,
                                           (size_t)nr, cudaMemcpyHostToDevice, s.st);
     if (e != cudaSuccess) { status = cuda_fail(e, "H2D"); return false; }
+    h2d_bytes += nr * cols * es;
     WinOut o{s.o_sum, reinterpret_cast<double*>(s.o_mean), reinterpret_cast<double*>(s.o_std), out_c};
     if (pipeline == SSB_PIPE_TABLE && sweep_ok) {  // table + windows without reading the table back
       e = launch_sat_sweep(in_dtype, band_in, nr, cols, cols, s.sat, sat_ld, w, stat_mask, o, s.ws, s.st, false);
@@ -951,6 +952,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     if (narrow ? (b >= 1 && !drain_band(b - 1)) : !drain_band(b)) break;
   }
   if (narrow && status == SSB_OK) drain_band(n_bands - 1);
+  t_host_h2d = h2d_bytes;
   if (d2h_st) {
     cudaError_t se = cudaStreamSynchronize(d2h_st);
     if (se != cudaSuccess && status == SSB_OK) status = cuda_fail(se, "stream sync");

@@ -64,7 +64,9 @@ def test_narrow_wire_matches_wide_and_oracle_u8(lib, band_rows, pitched):
         lib.ssb_host_wire(0)
         got, _, h2d, d2h = host_sum(lib, img, w, band_rows=band_rows, out_ld=ld, pipeline=pipe)
         assert np.array_equal(got, ref)
-        assert (h2d, d2h) == (img.size, 4 * n), "the sums must cross PCIe as uint32"
+        bands = 1 if band_rows == 0 else -(-(2300 - w + 1) // band_rows)  # every band uploads its own w - 1 extra rows
+        assert h2d == (2300 - w + 1 + bands * (w - 1)) * 2411
+        assert d2h == 4 * n, "the sums must cross PCIe as uint32"
         lib.ssb_host_wire(64)
         wide, _, _, d2h = host_sum(lib, img, w, band_rows=band_rows, out_ld=ld, pipeline=pipe)
         assert np.array_equal(wide, ref) and d2h == 8 * n

@@ -260,7 +260,7 @@ def test_c5_host_path_whole(sb, pool):
     assert got is hout or np.shares_memory(got, hout)
     h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
     lib.ssb_host_last_copy_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
-    assert h2d.value == 70000 * 85000
+    assert h2d.value == (out_r + 35 * 255) * 85000  # 35 bands of 2,048 output rows, each with its 255 extra input rows
     for lo in range(0, out_r, 4096):
         hi = min(out_r, lo + 4096)
         ref = O.swa_threaded(img[lo:hi + 255], 256, "sum", 1, P)
