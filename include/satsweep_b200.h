@@ -279,6 +279,16 @@ int ssb_host_release(void);
  * straight copy.  Returns the previous setting; other values only query. */
 int ssb_host_wire(int bits);
 
+/* Device-resident uint64 sums (rows x cols, contiguous, DEVICE pointer, e.g.
+ * the outputs of ssb_window_eval_multi / ssb_window_fused) into the caller's
+ * HOST uint64 array at pitch out_ld, through the narrow wire described at
+ * ssb_host_wire when max_sum -- an upper bound on every sum, e.g.
+ * w * w * max pixel; 0 = unknown -- is below 2^32 (multi_window and the other
+ * host-returning paths of api.py:58-67).  Waits for the work already queued on
+ * `stream`; returns when host_out is complete. */
+int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t max_sum, void* host_out, int64_t out_ld,
+                     void* stream);
+
 /* The host half of the narrow wire on its own: dst_u64[i] = src[i] for i < n,
  * zero-extended from src_bits = 16 or 32 (HOST pointers, any element
  * alignment; AVX2 streaming stores where the CPU has them).  No device work. */

@@ -99,6 +99,26 @@ def to_host(tensor, np_dtype: np.dtype) -> np.ndarray:
     return tensor.cpu().numpy().view(np.dtype(np_dtype))
 
 
+def sums_to_host(tensor, max_sum: int) -> np.ndarray:
+    """Device uint64 window sums -> fresh host uint64 array through ssb_sums_to_host: when
+    ``max_sum`` (a bound on every sum, w * w * the kind's largest pixel) is below 2**32 the
+    sums cross PCIe as uint32 / uint16 and the library's host threads widen them (the same
+    wire as ssb_swa_host); otherwise, and for small grids, a straight 64-bit copy."""
+    from . import _lib
+
+    if tensor.dim() != 2 or not tensor.is_contiguous() or tensor.element_size() != 8:
+        return to_host(tensor, np.uint64)
+    rows, cols = (int(v) for v in tensor.shape)
+    out = np.empty((rows, cols), dtype=np.uint64)
+    if rows == 0 or cols == 0:
+        return out
+    with torch().cuda.device(tensor.device):
+        rc = _lib.load().ssb_sums_to_host(tensor.data_ptr(), rows, cols, max(0, min(int(max_sum), 2**64 - 1)),
+                                          out.ctypes.data, cols, stream_ptr(tensor.device))
+    _lib.check(rc, "result read-back")
+    return out
+
+
 def as_np_view(tensor, np_dtype):
     """Device tensor with a different logical dtype (e.g. int64 storage read as uint64) -- host copy."""
     return to_host(tensor, np_dtype)

@@ -315,6 +315,16 @@ def _run_device(img: ImageGrid, w: int, stride: int, stats, pipeline: str, outs)
     return res
 
 
+def result_to_host(tensor, kind: ElemKind, stat: StatKind, w: int = 0) -> np.ndarray:
+    """A device result as the host array the reference returns (api.py:28-67).  Unsigned integer
+    sums with a known window go through the narrow wire (ssb_sums_to_host): their bound
+    w * w * max pixel decides whether they may cross PCIe as uint32 / uint16."""
+    dt = result_dtype(kind, stat)
+    if stat is StatKind.SUM and w > 0 and kind in (ElemKind.U8, ElemKind.U16):
+        return _device.sums_to_host(tensor, w * w * int(kind.max_value))
+    return _device.to_host(tensor, dt)
+
+
 def run_host(img: ImageGrid, w: int, stride: int, stats, pipeline: str = "auto", outs=None, band_rows: int = 0):
     """Host raster in, host results out, through the C-ABI streaming entry point ssb_swa_host."""
     lib = _lib.load()

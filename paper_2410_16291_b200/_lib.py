@@ -74,6 +74,7 @@ _SIGS = {
     "ssb_host_wire": (_int, [_int]),
     "ssb_host_threads": (_int, [_int]),
     "ssb_host_widen": (_int, [_vp, _int, _vp, _i64]),
+    "ssb_sums_to_host": (_int, [_vp, _i64, _i64, ctypes.c_uint64, _vp, _i64, _vp]),
     "ssb_host_last_copy_bytes": (None, [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "ssb_file_to_device": (_int, [ctypes.c_char_p, _i64, _i64, _vp, _int, _vp]),
     "ssb_device_to_file": (_int, [ctypes.c_char_p, _i64, _vp, _i64, _int, _vp]),

@@ -132,5 +132,5 @@ def multi_window(array, windows: list[int], stat: str = "sum", *, pipeline: str 
         _engine.check_nonfinite(flag)
         out = [r[kind] for r in res]
         if not img.on_device:
-            out = [_device.to_host(o, _engine.result_dtype(img.elem_kind, kind)) for o in out]
+            out = [_engine.result_to_host(o, img.elem_kind, kind, w) for o, w in zip(out, windows)]
         return out

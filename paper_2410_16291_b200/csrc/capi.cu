@@ -528,6 +528,36 @@ struct WirePipe {
     slot_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return true;
   }
+  // Enqueue one band's narrow results (nb rows at band_src, uint16 if `half`) on the copy stream, chunk by
+  // chunk into the ring (a slot is free once the chunk that held it is widened); each chunk is handed to
+  // the host threads when its copy lands.  dst: the band's first row in the caller's array.
+  // Returns cudaSuccess, a CUDA error, or cudaErrorUnknown when the host side stopped.
+  cudaError_t issue_band(cudaStream_t d2h_st, const char* band_src, bool half, int64_t nb, uint64_t* dst) {
+    const int esz = half ? 2 : 4;
+    const int64_t step = half ? 2 * rpc : rpc;  // the same bytes per chunk in either format
+    for (int64_t r0 = 0; r0 < nb; r0 += step) {
+      const int64_t g = issued.load(std::memory_order_relaxed), nr = r0 + step < nb ? step : nb - r0;
+      if (!wait_slot(g)) return cudaErrorUnknown;
+      const int slot = (int)(g % NS);
+      desc[slot] = Desc{dst + (size_t)r0 * out_ld, nr, half};
+      copied_bytes += nr * out_c * esz;
+      cudaError_t e = cudaMemcpyAsync(stage + (size_t)slot * slot_elems, band_src + (size_t)r0 * out_c * esz,
+                                      (size_t)nr * out_c * esz, cudaMemcpyDeviceToHost, d2h_st);
+      if (e == cudaSuccess) e = cudaEventRecord(copied[slot], d2h_st);
+      if (e != cudaSuccess) return e;
+      issued.store(g + 1, std::memory_order_release);
+    }
+    return cudaSuccess;
+  }
+  // threads from the call's settings; ring from the device's cache (or a temporary one); events; start
+  int threads_for_call() const {
+    static const int env_t = [] { const char* v = getenv("SSB_HOST_THREADS"); return v ? atoi(v) : 0; }();
+    static const int env_lws = [] { const char* v = getenv("LOCAL_WORLD_SIZE"); const int n = v ? atoi(v) : 1; return n < 1 ? 1 : n; }();
+    const int hw = (int)std::thread::hardware_concurrency() / env_lws;
+    const int set_t = g_host_threads.load();
+    const int t = set_t > 0 ? set_t : env_t > 0 ? env_t : (hw > 3 ? hw - 2 : 1);
+    return t > 64 ? 64 : t;
+  }
   // no more chunks: the threads leave once the issued ones are widened
   void finish(bool ok) {
     if (!ok) abort.store(true);
@@ -803,13 +833,8 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   if (narrow && status == SSB_OK) {
     // widening threads: ssb_host_threads(), else SSB_HOST_THREADS, else this process's share of the
     // cores (one process per GPU under torchrun: LOCAL_WORLD_SIZE) minus the issuing thread and the coordinator
-    static const int env_t = [] { const char* v = getenv("SSB_HOST_THREADS"); return v ? atoi(v) : 0; }();
-    static const int env_lws = [] { const char* v = getenv("LOCAL_WORLD_SIZE"); const int n = v ? atoi(v) : 1; return n < 1 ? 1 : n; }();
-    const int hw = (int)std::thread::hardware_concurrency() / env_lws;
-    const int set_t = g_host_threads.load();
     pipe.device = device;
-    pipe.T = set_t > 0 ? set_t : env_t > 0 ? env_t : (hw > 3 ? hw - 2 : 1);
-    if (pipe.T > 64) pipe.T = 64;
+    pipe.T = pipe.threads_for_call();
     pipe.out_c = out_c; pipe.out_ld = out_ld;
     static const int env_kb = [] { const char* v = getenv("SSB_HOST_CHUNK_KB"); return v ? atoi(v) : 0; }();
     pipe.plan((int64_t)(env_kb > 0 ? env_kb : 2048) * 256, band_rows);  // uint32 elements per chunk
@@ -911,7 +936,6 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
       // the narrowing kernel computed; the issuing thread runs ahead of the device, so this wait is short)
       if ((e = cudaEventSynchronize(s.ready)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
       const bool half = allow16 && h_max[b % n_sets] < 65536u;
-      const int esz = half ? 2 : 4;
       if (half) {  // the uint64 sums are dead once narrowed: their buffer takes the uint16 copy
         narrow_u32_u16_kernel<<<kNumSMs * 8, 256, 0, d2h_st>>>(reinterpret_cast<const uint32_t*>(s.o_n32),
                                                                reinterpret_cast<uint16_t*>(s.o_sum), nb * out_c);
@@ -919,22 +943,10 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
         if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
       }
       const char* band_src = reinterpret_cast<const char*>(half ? s.o_sum : s.o_n32);
-      // chunk by chunk into the staging ring (a slot is free once the chunk that held it is widened);
-      // each landed chunk is handed to the host threads
-      const int64_t step = half ? 2 * pipe.rpc : pipe.rpc;  // the same bytes per chunk in either format
-      for (int64_t r0 = 0; r0 < nb; r0 += step) {
-        const int64_t g = pipe.issued.load(std::memory_order_relaxed), nr = r0 + step < nb ? step : nb - r0;
-        if (!pipe.wait_slot(g)) { status = fail(SSB_ECUDA, "host widening stopped"); return false; }
-        const int slot = (int)(g % pipe.NS);
-        pipe.desc[slot] = WirePipe::Desc{reinterpret_cast<uint64_t*>(out_sum_host) + (size_t)(o0 + r0) * out_ld, nr, half};
-        pipe.copied_bytes += nr * out_c * esz;
-        if ((e = cudaMemcpyAsync(pipe.stage + (size_t)slot * pipe.slot_elems, band_src + (size_t)r0 * out_c * esz,
-                                 (size_t)nr * out_c * esz, cudaMemcpyDeviceToHost, d2h_st)) != cudaSuccess ||
-            (e = cudaEventRecord(pipe.copied[slot], d2h_st)) != cudaSuccess) {
-          status = cuda_fail(e, "D2H");
-          return false;
-        }
-        pipe.issued.store(g + 1, std::memory_order_release);
+      e = pipe.issue_band(d2h_st, band_src, half, nb, reinterpret_cast<uint64_t*>(out_sum_host) + (size_t)o0 * out_ld);
+      if (e != cudaSuccess) {
+        status = e == cudaErrorUnknown ? fail(SSB_ECUDA, "host widening stopped") : cuda_fail(e, "D2H");
+        return false;
       }
     }
     if (!d2h((stat_mask & SSB_SUM) && !narrow ? out_sum_host : nullptr, s.o_sum) ||
@@ -999,5 +1011,177 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   }
   return status;
 }
+
+// Device-resident uint64 sums -> the caller's host array through the narrow
+// wire of ssb_swa_host (multi_window and the other paths that evaluate on the
+// device and return host arrays, api.py:58-67): rows x cols contiguous on the
+// device, bands of ~32 M sums double-buffered through two narrowing buffers.
+int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t max_sum, void* host_out, int64_t out_ld,
+                     void* stream) {
+  if (!dev_sums || !host_out || rows < 1 || cols < 1 || out_ld < cols) return fail(SSB_EINVAL, "ssb_sums_to_host: bad arguments");
+  SSB_DEVICE_GUARD(stream);
+  cudaStream_t src_st = as_stream(stream);
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  const bool narrow = g_host_wire.load() != 64 && max_sum > 0 && max_sum < 4294967296ull && rows * cols >= (int64_t(1) << 22) &&
+                      (reinterpret_cast<uintptr_t>(dev_sums) & 15) == 0;
+  const bool allow16 = g_host_wire.load() != 32;
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(dev_sums);
+  if (!narrow) {  // the straight 64-bit copy
+    e = out_ld == cols ? cudaMemcpyAsync(host_out, src, (size_t)rows * cols * 8, cudaMemcpyDeviceToHost, src_st)
+                       : cudaMemcpy2DAsync(host_out, (size_t)out_ld * 8, src, (size_t)cols * 8, (size_t)cols * 8, (size_t)rows,
+                                           cudaMemcpyDeviceToHost, src_st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(src_st);
+    t_host_h2d = 0;
+    t_host_d2h = rows * cols * 8;
+    return e == cudaSuccess ? SSB_OK : cuda_fail(e, "ssb_sums_to_host");
+  }
+  // bands of whole rows whose first sum is 16-byte aligned (the narrowing kernels use 16-byte accesses)
+  int64_t band_rows = (int64_t(1) << 25) / cols;
+  if (band_rows < 2) band_rows = 2;
+  band_rows &= ~int64_t(1);
+  if (band_rows > rows) band_rows = rows;
+  const int64_t n_bands = (rows + band_rows - 1) / band_rows;
+  const int n_sets = n_bands < 2 ? 1 : 2;
+  struct Set {
+    void *n32 = nullptr, *n16 = nullptr;
+    uint32_t* d_max = nullptr;
+    cudaEvent_t ready = nullptr, drained = nullptr;
+  } sets[2];
+  int status = SSB_OK;
+  cudaStream_t work = nullptr, d2h_st = nullptr;
+  cudaEvent_t produced = nullptr;
+  cudaMemPool_t pool = nullptr;
+  if ((e = host_pool(device, &pool)) != cudaSuccess) return cuda_fail(e, "memory pool");
+  if ((e = cudaStreamCreateWithFlags(&work, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&d2h_st, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&produced, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventRecord(produced, src_st)) != cudaSuccess || (e = cudaStreamWaitEvent(work, produced, 0)) != cudaSuccess)
+    status = cuda_fail(e, "stream");
+  const size_t band_elems = (size_t)band_rows * cols;
+  for (int k = 0; k < n_sets && status == SSB_OK; ++k) {
+    Set& st = sets[k];
+    if ((e = cudaMallocFromPoolAsync(&st.n32, band_elems * 4, pool, work)) != cudaSuccess ||
+        (e = cudaMallocFromPoolAsync(&st.n16, band_elems * 2, pool, work)) != cudaSuccess ||
+        (e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&st.d_max), 256, pool, work)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&st.ready, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&st.drained, cudaEventDisableTiming)) != cudaSuccess)
+      status = cuda_fail(e, "device allocation");
+  }
+  WirePipe pipe;
+  StageCache* cache = nullptr;
+  void* own_stage = nullptr;
+  uint32_t* h_max = nullptr;
+  if (status == SSB_OK) {
+    pipe.device = device;
+    pipe.T = pipe.threads_for_call();
+    pipe.out_c = cols; pipe.out_ld = out_ld;
+    static const int env_kb = [] { const char* v = getenv("SSB_HOST_CHUNK_KB"); return v ? atoi(v) : 0; }();
+    pipe.plan((int64_t)(env_kb > 0 ? env_kb : 2048) * 256, band_rows);
+    pipe.NS = pipe.T + 4;
+    const size_t need = pipe.slot_elems * 4 * pipe.NS + 256;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      StageCache& c = g_stage[device];
+      if (!c.busy) {
+        if (c.bytes < need) {
+          if (c.p) cudaFreeHost(c.p);
+          c = StageCache{};
+          if ((e = cudaHostAlloc(&c.p, need, cudaHostAllocDefault)) == cudaSuccess) c.bytes = need;
+          else { c.p = nullptr; status = cuda_fail(e, "pinned staging"); }
+        }
+        if (c.p) { c.busy = true; cache = &c; pipe.stage = reinterpret_cast<uint32_t*>(c.p); }
+      }
+    }
+    if (!cache && status == SSB_OK) {
+      if ((e = cudaHostAlloc(&own_stage, need, cudaHostAllocDefault)) != cudaSuccess) status = cuda_fail(e, "pinned staging");
+      pipe.stage = reinterpret_cast<uint32_t*>(own_stage);
+    }
+    if (pipe.stage) h_max = pipe.stage + pipe.slot_elems * pipe.NS;
+    pipe.desc.assign(pipe.NS, WirePipe::Desc{});
+    pipe.copied.assign(pipe.NS, nullptr);
+    for (auto& ev : pipe.copied)
+      if (status == SSB_OK && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+        status = cuda_fail(e, "event");
+    if (status == SSB_OK) {
+      try {
+        pipe.start();
+      } catch (const std::exception& ex) {
+        pipe.finish(false);
+        status = fail(SSB_ECUDA, "host widening threads: %s", ex.what());
+      }
+    }
+  }
+  auto narrow_band = [&](int64_t b) -> bool {  // uint64 -> uint32 + the band's largest sum, on the work stream
+    Set& st = sets[b % n_sets];
+    const int64_t r0 = b * band_rows, nb = (r0 + band_rows < rows ? r0 + band_rows : rows) - r0;
+    if ((b >= n_sets && (e = cudaStreamWaitEvent(work, st.drained, 0)) != cudaSuccess) ||
+        (e = cudaMemsetAsync(st.d_max, 0, 4, work)) != cudaSuccess) {
+      status = cuda_fail(e, "narrow");
+      return false;
+    }
+    narrow_u64_u32_kernel<<<kNumSMs * 8, 256, 0, work>>>(src + (size_t)r0 * cols, reinterpret_cast<uint32_t*>(st.n32), nb * cols, st.d_max);
+    note_launch(1);
+    if ((e = cudaGetLastError()) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h_max + (b % n_sets), st.d_max, 4, cudaMemcpyDeviceToHost, work)) != cudaSuccess ||
+        (e = cudaEventRecord(st.ready, work)) != cudaSuccess) {
+      status = cuda_fail(e, "narrow");
+      return false;
+    }
+    return true;
+  };
+  auto drain_band = [&](int64_t b) -> bool {
+    Set& st = sets[b % n_sets];
+    const int64_t r0 = b * band_rows, nb = (r0 + band_rows < rows ? r0 + band_rows : rows) - r0;
+    if ((e = cudaStreamWaitEvent(d2h_st, st.ready, 0)) != cudaSuccess || (e = cudaEventSynchronize(st.ready)) != cudaSuccess) {
+      status = cuda_fail(e, "event");
+      return false;
+    }
+    const bool half = allow16 && h_max[b % n_sets] < 65536u;
+    if (half) {
+      narrow_u32_u16_kernel<<<kNumSMs * 8, 256, 0, d2h_st>>>(reinterpret_cast<const uint32_t*>(st.n32),
+                                                             reinterpret_cast<uint16_t*>(st.n16), nb * cols);
+      note_launch(1);
+      if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
+    }
+    e = pipe.issue_band(d2h_st, reinterpret_cast<const char*>(half ? st.n16 : st.n32), half, nb,
+                        reinterpret_cast<uint64_t*>(host_out) + (size_t)r0 * out_ld);
+    if (e == cudaSuccess) e = cudaEventRecord(st.drained, d2h_st);
+    if (e != cudaSuccess) {
+      status = e == cudaErrorUnknown ? fail(SSB_ECUDA, "host widening stopped") : cuda_fail(e, "D2H");
+      return false;
+    }
+    return true;
+  };
+  for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
+    if (!narrow_band(b)) break;
+    if (b >= 1 && !drain_band(b - 1)) break;
+  }
+  if (status == SSB_OK) drain_band(n_bands - 1);
+  if (d2h_st) { cudaStreamSynchronize(d2h_st); }
+  if (work) {
+    cudaStreamSynchronize(work);
+    for (auto& st : sets) {
+      void* ptrs[] = {st.n32, st.n16, st.d_max};
+      for (void* q : ptrs) if (q) cudaFreeAsync(q, work);
+      if (st.ready) cudaEventDestroy(st.ready);
+      if (st.drained) cudaEventDestroy(st.drained);
+    }
+    cudaStreamSynchronize(work);
+    cudaStreamDestroy(work);
+  }
+  if (d2h_st) cudaStreamDestroy(d2h_st);
+  if (produced) cudaEventDestroy(produced);
+  if (!pipe.threads.empty()) pipe.finish(status == SSB_OK);
+  if (pipe.coord_err != cudaSuccess && status == SSB_OK) status = cuda_fail(pipe.coord_err, "D2H wait");
+  for (auto ev : pipe.copied) if (ev) cudaEventDestroy(ev);
+  if (own_stage) cudaFreeHost(own_stage);
+  if (cache) { std::lock_guard<std::mutex> lk(g_pool_mu); cache->busy = false; }
+  t_host_h2d = 0;
+  t_host_d2h = pipe.copied_bytes;
+  return status;
+}
+
 
 }  // extern "C"

@@ -173,15 +173,15 @@ def swa_with_table(img: ImageGrid, win: WindowSpec, stat: StatKind) -> tuple[Int
     x, dev = _engine.device_input(img)
     sat, ld, outs = _engine.table_and_sweep(x, img.elem_kind, img.rows, img.cols, win.w, (stat,), dev)
     table = IntegralImage(sat, kind, (img.rows, img.cols), False, img.elem_kind, ld)
-    return table, ResultGrid(stat, _finish(img, (stat,), outs)[stat])
+    return table, ResultGrid(stat, _finish(img, (stat,), outs, win.w)[stat])
 
 
-def _finish(img: ImageGrid, stats, res) -> dict:
+def _finish(img: ImageGrid, stats, res, w: int = 0) -> dict:
     out = {}
     for s in stats:
         v = res[s]
         if not img.on_device:
-            v = _device.to_host(v, _engine.result_dtype(img.elem_kind, s))
+            v = _engine.result_to_host(v, img.elem_kind, s, w)
         out[s] = v
     return out
 
@@ -218,7 +218,7 @@ def _run_tables(img: ImageGrid, wins, stat: StatKind, force_table: bool = False)
         # one window: table and sweep in one pass (the table stays in scratch)
         _, _, outs = _engine.table_and_sweep(x, img.elem_kind, img.rows, img.cols, wins[0].w, (stat,), dev,
                                              scratch=True)
-        return [ResultGrid(stat, _finish(img, (stat,), outs)[stat])]
+        return [ResultGrid(stat, _finish(img, (stat,), outs, wins[0].w)[stat])]
     sat, sq, ld = _engine.build_tables(x, img.elem_kind, img.rows, img.cols, dev, squared=sq_needed, flag=flag,
                                        scratch=True)
     results = []
@@ -244,7 +244,7 @@ def _run_tables(img: ImageGrid, wins, stat: StatKind, force_table: bool = False)
             results.append(_engine.eval_tables(sat, sq, ld, img.elem_kind, img.rows, img.cols, win.w, win.stride,
                                                (stat,), dev))
     _engine.check_nonfinite(flag)
-    return [ResultGrid(stat, _finish(img, (stat,), r)[stat]) for r in results]
+    return [ResultGrid(stat, _finish(img, (stat,), r, w.w)[stat]) for r, w in zip(results, wins)]
 
 
 def swa_integral(img: ImageGrid, win: WindowSpec, stat: StatKind) -> ResultGrid:

@@ -158,3 +158,35 @@ def test_two_concurrent_calls_share_the_cores(lib):
     got = sb.swa(img, 64, "sum", devices=[0, 0])
     assert np.array_equal(got, O.swa(img, 64, "sum"))
     assert lib.ssb_host_threads(-1) == 0, "the per-call thread share must be restored"
+
+
+def test_sums_to_host_and_multi_window(lib):
+    """ssb_sums_to_host (device sums -> host uint64 through the narrow wire) against a plain copy, for
+    bounds on either side of 2^32 and 2^16, and multi_window(numpy) through it against the oracle."""
+    import torch
+
+    import paper_2410_16291_b200 as sb
+
+    lib.ssb_host_wire(0)
+    rng = np.random.default_rng(44)
+    h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
+    for rows, cols, hi in ((2500, 2301, 60000), (2500, 2301, 3_000_000_000), (33, 40, 100), (4097, 1025, 70000), (9001, 4000, 60000)):
+        vals = rng.integers(0, hi, size=(rows, cols), dtype=np.uint64)
+        dev = torch.from_numpy(vals.view(np.int64)).cuda()
+        for bound in (hi, 0, 2**40):
+            for ld in (cols, cols + 3):
+                out = np.full((rows, ld), 7, dtype=np.uint64)
+                rc = lib.ssb_sums_to_host(dev.data_ptr(), rows, cols, bound, out.ctypes.data, ld,
+                                          torch.cuda.current_stream().cuda_stream)
+                assert rc == 0
+                assert np.array_equal(out[:, :cols], vals) and (out[:, cols:] == 7).all()
+                lib.ssb_host_last_copy_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
+                narrow = bound == hi and rows * cols >= 1 << 22
+                width = 8 if not narrow else (2 if hi <= 65536 else 4)
+                assert d2h.value == rows * cols * width, (rows, cols, hi, bound, d2h.value)
+    img = (rng.random((2600, 2500)) < 0.1).astype(np.uint8)
+    ws = [25, 60, 300]
+    for pipe in ("auto", "table", "fused"):
+        got = sb.multi_window(img, ws, "sum", pipeline=pipe)
+        for g, w in zip(got, ws):
+            assert g.dtype == np.uint64 and np.array_equal(g, O.swa(img, w, "sum"))
