@@ -276,7 +276,9 @@ int ssb_host_release(void);
  * chunk into the caller's uint64 array: a half or a quarter of the PCIe
  * bytes, the same values; every other case copies 64-bit results straight
  * into the caller's array.  32: never narrower than uint32.  64: always the
- * straight copy.  Returns the previous setting; other values only query. */
+ * straight copy.  Returns the previous setting; other values only query.
+ * (At 0 and 32, 64-bit results bound for PAGEABLE host arrays also travel
+ * through the library's pinned ring, copied by the same host threads.) */
 int ssb_host_wire(int bits);
 
 /* Device-resident uint64 sums (rows x cols, contiguous, DEVICE pointer, e.g.

@@ -24,6 +24,7 @@
 namespace ssb {
 void widen_u32_to_u64(const uint32_t* src, uint64_t* dst, size_t n);  // host_widen.cpp
 void widen_u16_to_u64(const uint16_t* src, uint64_t* dst, size_t n);
+void copy_u64_stream(const uint64_t* src, uint64_t* dst, size_t n);
 }
 
 #ifndef SSB_ENONFINITE
@@ -444,13 +445,13 @@ struct WirePipe {
   struct Desc {           // what a ring slot holds; written before `issued`, read after `landed`
     uint64_t* dst = nullptr;  // first output row of the chunk in the caller's array
     int64_t rows = 0;
-    bool half = false;        // uint16 (else uint32)
+    int esz = 4;              // bytes per element on the wire: 2 / 4 (widened to uint64) or 8 (copied)
   };
   int device = 0, T = 1, NS = 1;  // workers, ring slots
   int64_t out_c = 0, out_ld = 0;
-  int64_t rpc = 1;                // output rows per uint32 chunk (a uint16 chunk takes twice as many: the same bytes)
+  int64_t rpc = 1;                // output rows per uint32 chunk (other widths take the rows that fill the same bytes)
   uint32_t* stage = nullptr;
-  size_t slot_elems = 0;          // uint32 elements per slot
+  size_t slot_elems = 0;          // uint32 elements per slot (a slot holds at least one 8-byte row)
   std::vector<Desc> desc;         // per slot
   int64_t copied_bytes = 0;       // device->host bytes of the narrow chunks (issuing thread)
   std::vector<cudaEvent_t> copied;  // per slot: the chunk's device->host copy has completed
@@ -469,8 +470,10 @@ struct WirePipe {
     rpc = chunk_elems / out_c;
     if (rpc < 1) rpc = 1;
     if (rpc > band_rows) rpc = band_rows;
+    if (rpc < 2) rpc = 2;  // room for one row of 8-byte elements
     slot_elems = (size_t)rpc * out_c;
   }
+  int64_t rows_per_chunk(int esz) const { const int64_t r = rpc * 4 / esz; return r < 1 ? 1 : r; }
   // waits until chunk g has reached `stage` (true) or no chunk g will come (false)
   bool wait_for(const std::atomic<int64_t>& stage_count, int64_t g) {
     for (;;) {
@@ -498,16 +501,16 @@ struct WirePipe {
         for (int64_t g = t; wait_for(landed, g); g += T) {
           const Desc d = desc[g % NS];
           const uint32_t* src = stage + (size_t)(g % NS) * slot_elems;
-          const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
           const auto t0 = std::chrono::steady_clock::now();
+          auto put = [&](size_t off, uint64_t* dst, size_t n) {  // n elements from element offset `off` of the slot
+            if (d.esz == 2) widen_u16_to_u64(reinterpret_cast<const uint16_t*>(src) + off, dst, n);
+            else if (d.esz == 4) widen_u32_to_u64(src + off, dst, n);
+            else copy_u64_stream(reinterpret_cast<const uint64_t*>(src) + off, dst, n);
+          };
           if (out_ld == out_c) {
-            if (d.half) widen_u16_to_u64(src16, d.dst, (size_t)d.rows * out_c);
-            else widen_u32_to_u64(src, d.dst, (size_t)d.rows * out_c);
+            put(0, d.dst, (size_t)d.rows * out_c);
           } else {
-            for (int64_t r = 0; r < d.rows; ++r) {
-              if (d.half) widen_u16_to_u64(src16 + (size_t)r * out_c, d.dst + (size_t)r * out_ld, (size_t)out_c);
-              else widen_u32_to_u64(src + (size_t)r * out_c, d.dst + (size_t)r * out_ld, (size_t)out_c);
-            }
+            for (int64_t r = 0; r < d.rows; ++r) put((size_t)r * out_c, d.dst + (size_t)r * out_ld, (size_t)out_c);
           }
           busy[t] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
           prog[t].store(g + 1, std::memory_order_release);
@@ -528,18 +531,17 @@ struct WirePipe {
     slot_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return true;
   }
-  // Enqueue one band's narrow results (nb rows at band_src, uint16 if `half`) on the copy stream, chunk by
+  // Enqueue one band's results (nb rows of esz-byte elements at band_src) on the copy stream, chunk by
   // chunk into the ring (a slot is free once the chunk that held it is widened); each chunk is handed to
   // the host threads when its copy lands.  dst: the band's first row in the caller's array.
   // Returns cudaSuccess, a CUDA error, or cudaErrorUnknown when the host side stopped.
-  cudaError_t issue_band(cudaStream_t d2h_st, const char* band_src, bool half, int64_t nb, uint64_t* dst) {
-    const int esz = half ? 2 : 4;
-    const int64_t step = half ? 2 * rpc : rpc;  // the same bytes per chunk in either format
+  cudaError_t issue_band(cudaStream_t d2h_st, const char* band_src, int esz, int64_t nb, uint64_t* dst) {
+    const int64_t step = rows_per_chunk(esz);  // about the same bytes per chunk in every format
     for (int64_t r0 = 0; r0 < nb; r0 += step) {
       const int64_t g = issued.load(std::memory_order_relaxed), nr = r0 + step < nb ? step : nb - r0;
       if (!wait_slot(g)) return cudaErrorUnknown;
       const int slot = (int)(g % NS);
-      desc[slot] = Desc{dst + (size_t)r0 * out_ld, nr, half};
+      desc[slot] = Desc{dst + (size_t)r0 * out_ld, nr, esz};
       copied_bytes += nr * out_c * esz;
       cudaError_t e = cudaMemcpyAsync(stage + (size_t)slot * slot_elems, band_src + (size_t)r0 * out_c * esz,
                                       (size_t)nr * out_c * esz, cudaMemcpyDeviceToHost, d2h_st);
@@ -782,8 +784,21 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
                       (double)w * (double)w * maxv < 4294967296.0 && out_r * out_c >= (int64_t(1) << 22);
   const bool allow16 = g_host_wire.load() != 32;
   uint32_t* h_max = nullptr;  // pinned: the bands' largest sums, one word per buffer set (tail of the ring)
+  // 64-bit results bound for pageable memory take the ring too (8-byte chunks, copied by the same
+  // threads): a DMA into pageable memory is staged by the driver at a fraction of the PCIe rate
+  auto pageable = [](const void* q) {
+    if (!q) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, q) != cudaSuccess) { cudaGetLastError(); return true; }
+    return a.type == cudaMemoryTypeUnregistered;
+  };
+  const bool stage_ok = g_host_wire.load() != 64 && out_r * out_c >= (int64_t(1) << 22);
+  const bool stage_sum = stage_ok && !narrow && (stat_mask & SSB_SUM) && pageable(out_sum_host);
+  const bool stage_mean = stage_ok && (stat_mask & SSB_MEAN) && pageable(out_mean_host);
+  const bool stage_std = stage_ok && (stat_mask & SSB_STD) && pageable(out_std_host);
+  const bool piped = narrow || stage_sum || stage_mean || stage_std;  // the ring and its threads are in use
+  int64_t d2h_direct = 0;  // bytes copied straight into the caller's arrays
   int64_t h2d_bytes = 0;  // uploaded: every band's input rows (consecutive bands share w - stride rows)
-  t_host_d2h = out_r * out_c * (8 * (nstats - 1) + ((stat_mask & SSB_SUM) ? (narrow ? 4 : 8) : 8));
 
   struct Set {
     cudaStream_t st = nullptr;         // H2D + compute of this set's bands
@@ -830,7 +845,7 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
   WirePipe pipe;
   StageCache* cache = nullptr;  // the device's cached ring when this call holds it
   void* own_stage = nullptr;    // a temporary ring otherwise
-  if (narrow && status == SSB_OK) {
+  if (piped && status == SSB_OK) {
     // widening threads: ssb_host_threads(), else SSB_HOST_THREADS, else this process's share of the
     // cores (one process per GPU under torchrun: LOCAL_WORLD_SIZE) minus the issuing thread and the coordinator
     pipe.device = device;
@@ -929,6 +944,17 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
                            : cudaMemcpy2DAsync(dst, (size_t)out_ld * 8, dev, (size_t)out_c * 8, (size_t)out_c * 8,
                                                (size_t)nb, cudaMemcpyDeviceToHost, d2h_st);
       if (ce != cudaSuccess) { status = cuda_fail(ce, "D2H"); return false; }
+      d2h_direct += nb * out_c * 8;
+      return true;
+    };
+    // 64-bit results: straight into pinned arrays, through the ring into pageable ones
+    auto out64 = [&](bool staged, void* host, void* dev) -> bool {
+      if (!host || !staged) return d2h(host, dev);
+      e = pipe.issue_band(d2h_st, reinterpret_cast<const char*>(dev), 8, nb, reinterpret_cast<uint64_t*>(host) + (size_t)o0 * out_ld);
+      if (e != cudaSuccess) {
+        status = e == cudaErrorUnknown ? fail(SSB_ECUDA, "host widening stopped") : cuda_fail(e, "D2H");
+        return false;
+      }
       return true;
     };
     if (narrow) {
@@ -943,27 +969,27 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
         if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
       }
       const char* band_src = reinterpret_cast<const char*>(half ? s.o_sum : s.o_n32);
-      e = pipe.issue_band(d2h_st, band_src, half, nb, reinterpret_cast<uint64_t*>(out_sum_host) + (size_t)o0 * out_ld);
+      e = pipe.issue_band(d2h_st, band_src, half ? 2 : 4, nb, reinterpret_cast<uint64_t*>(out_sum_host) + (size_t)o0 * out_ld);
       if (e != cudaSuccess) {
         status = e == cudaErrorUnknown ? fail(SSB_ECUDA, "host widening stopped") : cuda_fail(e, "D2H");
         return false;
       }
     }
-    if (!d2h((stat_mask & SSB_SUM) && !narrow ? out_sum_host : nullptr, s.o_sum) ||
-        !d2h((stat_mask & SSB_MEAN) ? out_mean_host : nullptr, s.o_mean) ||
-        !d2h((stat_mask & SSB_STD) ? out_std_host : nullptr, s.o_std))
+    if (!out64(stage_sum, (stat_mask & SSB_SUM) && !narrow ? out_sum_host : nullptr, s.o_sum) ||
+        !out64(stage_mean, (stat_mask & SSB_MEAN) ? out_mean_host : nullptr, s.o_mean) ||
+        !out64(stage_std, (stat_mask & SSB_STD) ? out_std_host : nullptr, s.o_std))
       return false;
     if ((e = cudaEventRecord(s.drained, d2h_st)) != cudaSuccess) { status = cuda_fail(e, "event"); return false; }
     return true;
   };
-  // The narrow wire's drain blocks the issuing thread on ring slots for about
+  // A drain through the ring blocks the issuing thread on ring slots for about
   // as long as the band's copy takes, so the next band's upload and kernels
   // are enqueued first; the straight copy never blocks.
   for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
     if (!compute_band(b)) break;
-    if (narrow ? (b >= 1 && !drain_band(b - 1)) : !drain_band(b)) break;
+    if (piped ? (b >= 1 && !drain_band(b - 1)) : !drain_band(b)) break;
   }
-  if (narrow && status == SSB_OK) drain_band(n_bands - 1);
+  if (piped && status == SSB_OK) drain_band(n_bands - 1);
   t_host_h2d = h2d_bytes;
   if (d2h_st) {
     cudaError_t se = cudaStreamSynchronize(d2h_st);
@@ -981,9 +1007,9 @@ int ssb_swa_host(const void* in_host, int in_dtype, int64_t rows, int64_t cols, 
     cudaStreamDestroy(s.st);
   }
   if (d2h_st) cudaStreamDestroy(d2h_st);
-  if (narrow) {
+  t_host_d2h = d2h_direct + pipe.copied_bytes;
+  if (piped) {
     if (!pipe.threads.empty()) pipe.finish(status == SSB_OK);  // joins after the last band is widened
-    t_host_d2h = out_r * out_c * 8 * (nstats - 1) + pipe.copied_bytes;
     if (pipe.coord_err != cudaSuccess && status == SSB_OK) status = cuda_fail(pipe.coord_err, "D2H wait");
     static const bool prof = getenv("SSB_HOST_PROF") != nullptr;  // tuning: where the host side spends its time
     if (prof && pipe.busy) {
@@ -1145,7 +1171,7 @@ int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t 
       note_launch(1);
       if ((e = cudaGetLastError()) != cudaSuccess) { status = cuda_fail(e, "narrow"); return false; }
     }
-    e = pipe.issue_band(d2h_st, reinterpret_cast<const char*>(half ? st.n16 : st.n32), half, nb,
+    e = pipe.issue_band(d2h_st, reinterpret_cast<const char*>(half ? st.n16 : st.n32), half ? 2 : 4, nb,
                         reinterpret_cast<uint64_t*>(host_out) + (size_t)r0 * out_ld);
     if (e == cudaSuccess) e = cudaEventRecord(st.drained, d2h_st);
     if (e != cudaSuccess) {

@@ -39,6 +39,19 @@ __attribute__((target("avx2"))) void widen16_avx2(const uint16_t* s, uint64_t* d
   for (; i < n; ++i) d[i] = s[i];
 }
 
+__attribute__((target("avx2"))) void copy64_avx2(const uint64_t* s, uint64_t* d, size_t n) {
+  size_t i = 0;
+  for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = s[i];
+  for (; i + 8 <= n; i += 8) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 4));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 4), b);
+  }
+  _mm_sfence();
+  for (; i < n; ++i) d[i] = s[i];
+}
+
 template <typename T>
 void widen_plain(const T* s, uint64_t* d, size_t n) {
   for (size_t i = 0; i < n; ++i) d[i] = s[i];
@@ -58,4 +71,13 @@ void widen_u16_to_u64(const uint16_t* src, uint64_t* dst, size_t n) {
   else widen_plain(src, dst, n);
 }
 
+}  // namespace ssb
+
+// 8-byte results (float64 mean / std, wide sums) from the pinned ring into pageable memory
+namespace ssb {
+void copy_u64_stream(const uint64_t* src, uint64_t* dst, size_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) copy64_avx2(src, dst, n);
+  else widen_plain(src, dst, n);
+}
 }  // namespace ssb

@@ -190,3 +190,34 @@ def test_sums_to_host_and_multi_window(lib):
         got = sb.multi_window(img, ws, "sum", pipeline=pipe)
         for g, w in zip(got, ws):
             assert g.dtype == np.uint64 and np.array_equal(g, O.swa(img, w, "sum"))
+
+
+def test_pageable_float_results_take_the_ring(lib):
+    """float64 mean / std bound for pageable arrays go through the pinned ring in 8-byte chunks (copied,
+    not widened): bit-identical to the straight copy, same bytes over PCIe, pitched or not, several bands."""
+    from paper_2410_16291_b200 import _lib
+
+    rng = np.random.default_rng(8)
+    img = rng.lognormal(0.0, 1.0, size=(2300, 2400)).astype(np.float32)
+    w = 33
+    out_r, out_c = 2300 - w + 1, 2400 - w + 1
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    res = {}
+    for bits in (0, 64):
+        lib.ssb_host_wire(bits)
+        for ld, br in ((out_c, 0), (out_c + 3, 500)):
+            mean = np.full((out_r, ld), -1.0)
+            std = np.full((out_r, ld), -1.0)
+            rc = lib.ssb_swa_host(vp(img), _lib.F32, 2300, 2400, 2400, w, 1, _lib.MEAN | _lib.STD, None, vp(mean), vp(std),
+                                  ld, _lib.PIPE_FUSED, 0, br)
+            _lib.check(rc, "ssb_swa_host")
+            h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
+            lib.ssb_host_last_copy_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
+            assert d2h.value == 16 * out_r * out_c
+            assert (mean[:, out_c:] == -1.0).all() and (std[:, out_c:] == -1.0).all()
+            res[bits, ld] = (mean[:, :out_c].copy(), std[:, :out_c].copy())
+    lib.ssb_host_wire(0)
+    for ld in (out_c, out_c + 3):
+        assert np.array_equal(res[0, ld][0], res[64, ld][0]) and np.array_equal(res[0, ld][1], res[64, ld][1])
+    np.testing.assert_allclose(res[0, out_c][0], O.swa(img, w, "mean"), rtol=1e-6)
+    np.testing.assert_allclose(res[0, out_c][1], O.swa(img, w, "std"), rtol=1e-6, atol=1e-9)
