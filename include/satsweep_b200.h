@@ -286,8 +286,10 @@ int ssb_host_wire(int bits);
  * HOST uint64 array at pitch out_ld, through the narrow wire described at
  * ssb_host_wire when max_sum -- an upper bound on every sum, e.g.
  * w * w * max pixel; 0 = unknown -- is below 2^32 (multi_window and the other
- * host-returning paths of api.py:58-67).  Waits for the work already queued on
- * `stream`; returns when host_out is complete. */
+ * host-returning paths of api.py:58-67).  Any other contiguous 8-byte results
+ * (max_sum = 0: float64 mean / std, wide sums) bound for a pageable array are
+ * copied through the same ring as they are.  Waits for the work already
+ * queued on `stream`; returns when host_out is complete. */
 int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t max_sum, void* host_out, int64_t out_ld,
                      void* stream);
 

@@ -322,6 +322,8 @@ def result_to_host(tensor, kind: ElemKind, stat: StatKind, w: int = 0) -> np.nda
     dt = result_dtype(kind, stat)
     if stat is StatKind.SUM and w > 0 and kind in (ElemKind.U8, ElemKind.U16):
         return _device.sums_to_host(tensor, w * w * int(kind.max_value))
+    if np.dtype(dt).itemsize == 8:  # float64 / int64: no bound, copied through the ring as they are
+        return _device.sums_to_host(tensor, 0).view(np.dtype(dt))
     return _device.to_host(tensor, dt)
 
 

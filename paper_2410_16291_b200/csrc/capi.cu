@@ -1050,11 +1050,19 @@ int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t 
   int device = 0;
   cudaError_t e = cudaGetDevice(&device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const bool narrow = g_host_wire.load() != 64 && max_sum > 0 && max_sum < 4294967296ull && rows * cols >= (int64_t(1) << 22) &&
-                      (reinterpret_cast<uintptr_t>(dev_sums) & 15) == 0;
+  const bool stage_ok = g_host_wire.load() != 64 && rows * cols >= (int64_t(1) << 22);
+  const bool narrow = stage_ok && max_sum > 0 && max_sum < 4294967296ull && (reinterpret_cast<uintptr_t>(dev_sums) & 15) == 0;
   const bool allow16 = g_host_wire.load() != 32;
   const uint64_t* src = reinterpret_cast<const uint64_t*>(dev_sums);
-  if (!narrow) {  // the straight 64-bit copy
+  // 8-byte values without a 32-bit bound (float64 results, wide sums) bound for pageable memory: through the
+  // ring as they are, copied out by the host threads
+  bool staged64 = false;
+  if (stage_ok && !narrow) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, host_out) != cudaSuccess) { cudaGetLastError(); staged64 = true; }
+    else staged64 = a.type == cudaMemoryTypeUnregistered;
+  }
+  if (!narrow && !staged64) {  // the straight 64-bit copy
     e = out_ld == cols ? cudaMemcpyAsync(host_out, src, (size_t)rows * cols * 8, cudaMemcpyDeviceToHost, src_st)
                        : cudaMemcpy2DAsync(host_out, (size_t)out_ld * 8, src, (size_t)cols * 8, (size_t)cols * 8, (size_t)rows,
                                            cudaMemcpyDeviceToHost, src_st);
@@ -1067,9 +1075,9 @@ int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t 
   int64_t band_rows = (int64_t(1) << 25) / cols;
   if (band_rows < 2) band_rows = 2;
   band_rows &= ~int64_t(1);
-  if (band_rows > rows) band_rows = rows;
+  if (band_rows > rows || !narrow) band_rows = rows;
   const int64_t n_bands = (rows + band_rows - 1) / band_rows;
-  const int n_sets = n_bands < 2 ? 1 : 2;
+  const int n_sets = !narrow ? 0 : n_bands < 2 ? 1 : 2;
   struct Set {
     void *n32 = nullptr, *n16 = nullptr;
     uint32_t* d_max = nullptr;
@@ -1083,7 +1091,8 @@ int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t 
   if ((e = cudaStreamCreateWithFlags(&work, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&d2h_st, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&produced, cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaEventRecord(produced, src_st)) != cudaSuccess || (e = cudaStreamWaitEvent(work, produced, 0)) != cudaSuccess)
+      (e = cudaEventRecord(produced, src_st)) != cudaSuccess || (e = cudaStreamWaitEvent(work, produced, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(d2h_st, produced, 0)) != cudaSuccess)
     status = cuda_fail(e, "stream");
   const size_t band_elems = (size_t)band_rows * cols;
   for (int k = 0; k < n_sets && status == SSB_OK; ++k) {
@@ -1180,11 +1189,16 @@ int ssb_sums_to_host(const void* dev_sums, int64_t rows, int64_t cols, uint64_t 
     }
     return true;
   };
-  for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
-    if (!narrow_band(b)) break;
-    if (b >= 1 && !drain_band(b - 1)) break;
+  if (narrow) {
+    for (int64_t b = 0; status == SSB_OK && b < n_bands; ++b) {
+      if (!narrow_band(b)) break;
+      if (b >= 1 && !drain_band(b - 1)) break;
+    }
+    if (status == SSB_OK) drain_band(n_bands - 1);
+  } else if (status == SSB_OK) {  // staged64: the array as it is
+    e = pipe.issue_band(d2h_st, reinterpret_cast<const char*>(src), 8, rows, reinterpret_cast<uint64_t*>(host_out));
+    if (e != cudaSuccess) status = e == cudaErrorUnknown ? fail(SSB_ECUDA, "host copy stopped") : cuda_fail(e, "D2H");
   }
-  if (status == SSB_OK) drain_band(n_bands - 1);
   if (d2h_st) { cudaStreamSynchronize(d2h_st); }
   if (work) {
     cudaStreamSynchronize(work);

@@ -190,6 +190,9 @@ def test_sums_to_host_and_multi_window(lib):
         got = sb.multi_window(img, ws, "sum", pipeline=pipe)
         for g, w in zip(got, ws):
             assert g.dtype == np.uint64 and np.array_equal(g, O.swa(img, w, "sum"))
+    got = sb.multi_window(img, ws, "mean")  # float64 results: through the ring as they are
+    for g, w in zip(got, ws):
+        assert g.dtype == np.float64 and np.array_equal(g, O.swa(img, w, "mean"))
 
 
 def test_pageable_float_results_take_the_ring(lib):
